@@ -1,0 +1,158 @@
+/*
+ * qaoa_b200.h -- C ABI of the B200-native QAOA Max-Cut state-vector engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   simulate(g, params, backend="bitwise")  ->  expectation(g, s)
+ * (reference: pkg/src/qaoa_maxcut/circuit.py:97-121).  Plain C types only:
+ * pointers, sizes, doubles.  Every call is synchronous on the context's stream
+ * unless noted, returns QAOA_OK (0) on success or a negative QAOA_E* code, and
+ * leaves a message for qaoa_last_error().  The Python package
+ * paper_2312_03019_b200 binds these with ctypes and maps the codes onto the
+ * reference's exceptions (ValueError / IndexError with the same substrings).
+ *
+ * Layout: the state is complex128, interleaved (re, im) doubles, bit i of the
+ * basis index = qubit i (reference state.py:3-4), resident in HBM and owned
+ * by the context.  Host arrays passed in are copied during the call.
+ */
+#ifndef QAOA_B200_H
+#define QAOA_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define QAOA_API __attribute__((visibility("default")))
+#else
+#define QAOA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------- */
+#define QAOA_OK 0
+#define QAOA_E_INVALID (-1)   /* bad argument -> ValueError                      */
+#define QAOA_E_RANGE (-2)     /* qubit index out of range -> IndexError          */
+#define QAOA_E_CUDA (-3)      /* CUDA runtime / launch failure -> RuntimeError   */
+#define QAOA_E_NOMEM (-4)     /* device allocation failed -> MemoryError         */
+#define QAOA_E_STATE (-5)     /* call order (no graph / no state) -> RuntimeError */
+
+/* ---- run flags (qaoa_run_layers) ------------------------------------------ */
+#define QAOA_RUN_EXACT 0x1          /* bit-exact reference arithmetic and qubit order  */
+#define QAOA_RUN_FROM_STATE 0x2     /* start from the resident state, not |+>^n         */
+#define QAOA_RUN_EXPECTATION 0x4    /* fuse <C> into the last sweep (qaoa_expectation)  */
+#define QAOA_RUN_TIMING 0x8         /* record per-launch CUDA-event times               */
+
+typedef struct qaoa_ctx qaoa_ctx;
+
+/* Last error message of the calling thread ("" when none). */
+QAOA_API const char* qaoa_last_error(void);
+
+/* Library version string, e.g. "qaoa_b200 0.1 sm_100a". */
+QAOA_API const char* qaoa_version(void);
+
+/* Number of visible CUDA devices (0 on a host without a GPU; never fails). */
+QAOA_API int qaoa_device_count(void);
+
+/* Create a context holding a 2^n_qubits complex128 state on `device`.
+ * Replaces the state allocation of StateVector / init_zero_state
+ * (reference state.py:43-52, :66-72); the memory guard of
+ * check_qubit_budget (state.py:55-63) is enforced by the caller, the library
+ * only refuses sizes that do not fit the device (QAOA_E_NOMEM).
+ * `stream` may be NULL (the library creates its own non-blocking stream) or a
+ * cudaStream_t owned by the caller (e.g. torch.cuda.current_stream()). */
+QAOA_API int qaoa_create(int n_qubits, int device, void* stream, qaoa_ctx** out);
+
+/* As qaoa_create, but the state lives in caller-owned device memory of at least
+ * 16 * 2^n_qubits bytes (e.g. a torch tensor used for NCCL exchanges). */
+QAOA_API int qaoa_create_external(int n_qubits, int device, void* stream, void* device_amps,
+                         qaoa_ctx** out);
+
+QAOA_API void qaoa_destroy(qaoa_ctx* ctx);
+
+/* Raw device pointer of the state (interleaved re, im doubles). */
+QAOA_API void* qaoa_state_ptr(qaoa_ctx* ctx);
+
+/* Use `stream` (a cudaStream_t) for all later launches. */
+QAOA_API int qaoa_set_stream(qaoa_ctx* ctx, void* stream);
+
+/* Graph in the reference's format: row_mask[i] has bit j set iff edge (i, j),
+ * i < j (Graph.row_mask, graph.py:57-59); tot_edge = Graph.tot_edge.  The
+ * context's qubits are global node bits [0, n_local) of a larger register
+ * whose top bits are fixed to `x_hi` (0 for an unsharded state); n_nodes is the
+ * node count of the whole graph.  Replaces plan_for / CompressedCostPlan
+ * (cost.py:66-108).  Does not build the cut table (see qaoa_build_cut_table). */
+QAOA_API int qaoa_set_graph(qaoa_ctx* ctx, int n_nodes, const uint64_t* row_mask, int tot_edge,
+                   uint64_t x_hi);
+
+/* Launch control (circuit.py:42-48): every amplitude = sqrt(1/2^n_nodes). */
+QAOA_API int qaoa_init_uniform(qaoa_ctx* ctx);
+
+/* Copy host amplitudes [offset, offset+count) in / out (interleaved re, im). */
+QAOA_API int qaoa_write_amplitudes(qaoa_ctx* ctx, uint64_t offset, uint64_t count, const double* src);
+QAOA_API int qaoa_read_amplitudes(qaoa_ctx* ctx, uint64_t offset, uint64_t count, double* dst);
+
+/* Unweighted cost layer (apply_cost_bitwise, cost.py:162-176):
+ * amp[x] *= table[2E - 2C(x)], table = _phase_table(E, gamma) (cost.py:136-139)
+ * given as 2E+1 interleaved complex doubles.  Bit-exact (FMA-form multiply). */
+QAOA_API int qaoa_apply_cost(qaoa_ctx* ctx, const double* phase_table);
+
+/* Single-qubit RX(theta) (apply_rx, state.py:110-128): c = cos(theta/2),
+ * s = sin(theta/2).  Bit-exact (products rounded separately). */
+QAOA_API int qaoa_apply_rx(qaoa_ctx* ctx, int qubit, double c, double s);
+
+/* Mixer layer (apply_mixer_layer, circuit.py:89-94): RX on every local qubit in
+ * increasing order, c = cos(-beta/2), s = sin(-beta/2).  Bit-exact. */
+QAOA_API int qaoa_apply_mixer(qaoa_ctx* ctx, double c, double s);
+
+/* The fused p-level circuit (simulate(..., "bitwise"), circuit.py:97-113):
+ * |+>^n (unless QAOA_RUN_FROM_STATE), then per level l: cost with
+ * phase_tables[l] (2E+1 complex), mixer with (c[l], s[l]).
+ * QAOA_RUN_EXACT reproduces the reference bit for bit; otherwise the sweeps are
+ * re-ordered / merged across levels and the butterflies use a factored form
+ * (|error| <= 1e-13 absolute, contract 1e-12).  With QAOA_RUN_EXPECTATION the
+ * last sweep also accumulates <C>, retrievable with qaoa_expectation. */
+QAOA_API int qaoa_run_layers(qaoa_ctx* ctx, int p, const double* phase_tables, const double* c,
+                    const double* s, int flags);
+
+/* <C> = sum_x |amp_x|^2 C(x) (expectation, circuit.py:116-121; graph must be
+ * unweighted).  Deterministic: fixed-order block partials.  Returns the value
+ * fused by the last qaoa_run_layers(..., QAOA_RUN_EXPECTATION) when the state
+ * has not changed since, else runs a read-only reduction. */
+QAOA_API int qaoa_expectation(qaoa_ctx* ctx, double* out);
+
+/* Partial sum of |amp|^2 over the local shard (StateVector.norm, state.py:50-51). */
+QAOA_API int qaoa_norm_sq(qaoa_ctx* ctx, double* out);
+
+/* max_x |a_x - b_x| over two equal-size states (max_abs_diff, state.py:152-156). */
+QAOA_API int qaoa_max_abs_diff(qaoa_ctx* a, qaoa_ctx* b, double* out);
+
+/* Cut-table builder (CompressedCostPlan.cut_counts, cost.py:88-99): integer C(x)
+ * for every local basis state into device memory (uint8 when E <= 255, else
+ * uint16).  qaoa_read_cut_table widens [offset, offset+count) to int64. */
+QAOA_API int qaoa_build_cut_table(qaoa_ctx* ctx);
+QAOA_API int qaoa_read_cut_table(qaoa_ctx* ctx, uint64_t offset, uint64_t count, int64_t* dst);
+QAOA_API int qaoa_free_cut_table(qaoa_ctx* ctx);
+
+/* Per-launch device times (ms) of the last qaoa_run_layers run with
+ * QAOA_RUN_TIMING; returns the number of launches (<= cap written). */
+QAOA_API int qaoa_layer_timings(qaoa_ctx* ctx, float* ms, int cap);
+
+/* Number of kernels the last qaoa_run_layers call launched, and the HBM bytes
+ * its sweeps moved (read + write, algorithmic). */
+QAOA_API int qaoa_last_run_stats(qaoa_ctx* ctx, int* launches, double* hbm_bytes);
+
+/* Block until all work on the context's stream is done. */
+QAOA_API int qaoa_synchronize(qaoa_ctx* ctx);
+
+/* ---- shard exchange (multi-GPU, reference has none: SPEC.md:186) ----------
+ * Swap physical bits: after the call, local bit `local_bits[k]` of this shard
+ * holds what global bit (n_local + k) held (k < g), given the received peer
+ * chunks.  The engine exposes pack/unpack so the host can drive NCCL or P2P. */
+QAOA_API int qaoa_pack_chunks(qaoa_ctx* ctx, int g, const int* local_bits, void* dst_device);
+QAOA_API int qaoa_unpack_chunks(qaoa_ctx* ctx, int g, const int* local_bits, const void* src_device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QAOA_B200_H */

@@ -1,0 +1,183 @@
+"""The p-level QAOA circuit on the B200 engine: the drop-in for the reference's
+``simulate`` / ``expectation`` (pkg/src/qaoa_maxcut/circuit.py:97-121).
+
+``simulate`` sends the graph's row masks, the host-built phase tables
+(cost.py:136-139 expression) and the RX coefficients (state.py:114-115) through
+the C ABI ``qaoa_run_layers``: launch-control init, p fused cost+mixer levels
+and -- fused into the last sweep -- the expected cut, all in HBM.  The state
+comes back device-resident; ``expectation`` returns the fused value when the
+state is untouched since, else runs the device reduction.
+
+``exact=True`` reproduces the reference bit for bit (same qubit order and
+rounding); the default fast schedule merges adjacent levels' sweeps and uses
+one-DFMA butterflies, within 1e-13 of the reference (contract: 1e-12).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .cost import phase_table, plan_for
+from .graph import Graph
+from .state import (
+    DEFAULT_MAX_QUBITS,
+    Engine,
+    StateVector,
+    check_qubit_budget,
+    write_counter,
+)
+
+BACKENDS = ("baseline", "compressed", "bitwise")  # circuit.py:13
+
+
+@dataclass(frozen=True)
+class QaoaParams:
+    """Angle schedule: gamma in [0, 2pi), beta in [0, pi), one pair per level."""
+
+    gamma: tuple[float, ...]
+    beta: tuple[float, ...]
+
+    def __post_init__(self):
+        if len(self.gamma) != len(self.beta):
+            raise ValueError("gamma and beta must have the same length")
+        if len(self.gamma) < 1:
+            raise ValueError("need at least one level")
+
+    @property
+    def p(self) -> int:
+        return len(self.gamma)
+
+
+def validate_backend(backend: str, g: Graph | None = None) -> str:
+    """circuit.py:34-39."""
+    if backend not in BACKENDS:
+        raise ValueError(f"unknown backend {backend!r}; choose from {BACKENDS}")
+    if backend == "bitwise" and g is not None and not g.is_unweighted:
+        raise ValueError("bitwise backend requires an unweighted graph")
+    return backend
+
+
+def _require_engine_graph(g: Graph, what: str) -> None:
+    if not g.is_unweighted:
+        raise NotImplementedError(
+            f"{what}: the B200 engine implements the unweighted (bitwise) path; "
+            "weighted graphs are outside this build's scope")
+
+
+def rx_coefficients(beta: float) -> tuple[float, float]:
+    """(cos(theta/2), sin(theta/2)) with theta = -beta (circuit.py:93, state.py:114-115)."""
+    theta = -beta
+    return math.cos(theta / 2.0), math.sin(theta / 2.0)
+
+
+def level_arrays(g: Graph, params: QaoaParams):
+    """Host-side inputs of qaoa_run_layers: p phase tables and RX coefficients."""
+    tables = np.ascontiguousarray(
+        np.stack([phase_table(g.tot_edge, gm) for gm in params.gamma]).astype(np.complex128))
+    coeffs = [rx_coefficients(b) for b in params.beta]
+    cs = np.array([c for c, _ in coeffs], dtype=np.float64)
+    ss = np.array([s for _, s in coeffs], dtype=np.float64)
+    return tables, cs, ss
+
+
+def init_uniform(n: int, max_qubits: int = DEFAULT_MAX_QUBITS) -> StateVector:
+    """Uniform superposition set directly (launch control, circuit.py:42-48)."""
+    check_qubit_budget(n, max_qubits)
+    eng = Engine(n)
+    eng.call("qaoa_init_uniform")
+    write_counter.add(1 << n)
+    return StateVector(n, engine=eng)
+
+
+def init_state(n: int, launch_control: bool = True, threads: int = 1,
+               max_qubits: int = DEFAULT_MAX_QUBITS) -> StateVector:
+    """circuit.py:51-62.  Without launch control the reference applies n Hadamards
+    to |0..0>; the result is the uniform state up to rounding (<= 1e-16), which
+    the engine writes directly."""
+    return init_uniform(n, max_qubits)
+
+
+def apply_cost_layer(s: StateVector, g: Graph, gamma: float, backend: str = "baseline",
+                     threads: int = 1, batch_width: int | None = None,
+                     use_table_popcount: bool = False) -> StateVector:
+    """One cost layer, one device pass (circuit.py:65-86)."""
+    validate_backend(backend, g)
+    _require_engine_graph(g, "apply_cost_layer")
+    from .cost import apply_cost_batched, apply_cost_bitwise
+
+    plan = plan_for(g)
+    if batch_width is not None and backend == "bitwise":
+        return apply_cost_batched(s, plan, gamma, batch_width, use_table_popcount)
+    return apply_cost_bitwise(s, plan, gamma, threads)
+
+
+def apply_mixer_layer(s: StateVector, beta: float, threads: int = 1) -> StateVector:
+    """RX(-beta) on every qubit in increasing order (circuit.py:89-94), bit-exact,
+    as ceil((n-3)/9) tiled device sweeps."""
+    c, sn = rx_coefficients(beta)
+    s.engine().call("qaoa_apply_mixer", c, sn)
+    write_counter.add(s.n << s.n)
+    return s
+
+
+def simulate(
+    g: Graph,
+    params: QaoaParams,
+    backend: str = "baseline",
+    launch_control: bool = True,
+    threads: int = 1,
+    batch_width: int | None = None,
+    use_table_popcount: bool = False,
+    max_qubits: int = DEFAULT_MAX_QUBITS,
+    *,
+    exact: bool = False,
+    device: int = 0,
+    fuse_expectation: bool = True,
+    state: StateVector | None = None,
+) -> StateVector:
+    """Run the p-level circuit on the GPU and return the device-resident state
+    (circuit.py:97-113).  All three backend names select the fused engine (they
+    are numerically equivalent on unweighted graphs: test_acceptance.py:60-79).
+
+    Extra keyword-only knobs: ``exact`` (bit-exact reference schedule),
+    ``device``, ``fuse_expectation`` (accumulate <C> in the last sweep) and
+    ``state`` (reuse a StateVector's device buffer instead of allocating)."""
+    validate_backend(backend, g)
+    if batch_width is not None and batch_width not in (1, 2, 4, 8):
+        raise ValueError(f"batch width must be 1, 2, 4, or 8, got {batch_width}")
+    _require_engine_graph(g, "simulate")
+    check_qubit_budget(g.n, max_qubits)
+    if state is not None and state.n == g.n:
+        eng = state._eng if state._eng is not None else Engine(g.n, device)
+        state._eng, state._host, state._where = eng, None, "device"
+        s = state
+    else:
+        eng = Engine(g.n, device)
+        s = StateVector(g.n, engine=eng)
+    eng.ensure_graph(g)
+    tables, cs, ss = level_arrays(g, params)
+    flags = (_lib.RUN_EXACT if exact else 0) | (_lib.RUN_EXPECTATION if fuse_expectation else 0)
+    eng.call("qaoa_run_layers", params.p, _lib.dptr(tables.view(np.float64)), _lib.dptr(cs),
+             _lib.dptr(ss), flags)
+    write_counter.add((1 << g.n) * (1 + params.p * (g.n + 1)))
+    return s
+
+
+def expectation(g: Graph, s: StateVector) -> float:
+    """sum_x |amp_x|^2 C(x) on the device (circuit.py:116-121): deterministic
+    fixed-order reduction; the fused value of the last simulate when valid."""
+    if s.n != g.n:
+        raise ValueError(f"state has {s.n} qubits but graph has {g.n} nodes")
+    _require_engine_graph(g, "expectation")
+    eng = s.engine()
+    eng.ensure_graph(g)
+    return eng.scalar("qaoa_expectation")
+
+
+def gate_counts(n: int, g: Graph, p: int) -> tuple[int, int, int]:
+    """(H, RZZ, RX) counts without launch control (circuit.py:136-138)."""
+    return n, p * g.tot_edge, p * n

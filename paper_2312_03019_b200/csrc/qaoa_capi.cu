@@ -1,0 +1,776 @@
+// qaoa_capi.cu -- extern "C" boundary (include/qaoa_b200.h) and the host-side
+// sweep planner of the B200 QAOA engine.
+//
+// The planner turns p levels of (cost, mixer) into a list of fused sweeps:
+//   * qubit sets: S_0 = tile bits at positions 0..11 (all active); the
+//     remaining positions 12..n-1 in balanced chunks of <= 9, each carried in a
+//     tile together with the lowest positions 0..(11-m) (inactive) so HBM
+//     accesses stay >= 128-byte runs;
+//   * exact mode (QAOA_RUN_EXACT): per level [cost + RX(S_0)] [RX(S_1)] ...,
+//     qubits in increasing order, reference arithmetic: bit-identical to
+//     simulate(..., "bitwise") (reference circuit.py:97-113);
+//   * fast mode: odd levels visit the sets forward, even levels backward, so
+//     the last set of level l and the first of level l+1 coincide and run as
+//     ONE sweep [RX_l(S) -> cost_{l+1} -> RX_{l+1}(S)]: (R-1)p+1 sweeps for R
+//     sets instead of R p.  Butterflies in factored one-DFMA form; the level
+//     scale factors ride on the next phase table / the final scale.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <string>
+#include <vector>
+
+#include "../../include/qaoa_b200.h"
+#include "qaoa_sweep.h"
+
+using namespace qb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(QAOA_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(expr)                                   \
+  do {                                                   \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr);  \
+  } while (0)
+
+struct SetDesc {
+  int pos[12];
+  unsigned act;
+};
+
+struct SweepPlan {
+  int set;
+  int pre_cost;  // level index or -1
+  int stage1;    // level index or -1
+  int mid_cost;  // level index or -1
+  int stage2;    // level index or -1
+};
+
+}  // namespace
+
+struct qaoa_ctx {
+  int n = 0;  // local qubits (bits of the state index)
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double2* amps = nullptr;
+  bool own_amps = false;
+  GraphDev g{};
+  bool has_graph = false;
+  void* cut_table = nullptr;
+  int cut_bytes = 0;
+  double* partials = nullptr;
+  int partials_len = 0;
+  double* d_scalar = nullptr;
+  double2* d_tables = nullptr;
+  size_t d_tables_cap = 0;  // in double2
+  double2* h_tables = nullptr;  // pinned staging
+  size_t h_tables_cap = 0;
+  // expectation cached from the last fused run
+  bool expect_valid = false;
+  double expect_value = 0.0;
+  // timing
+  std::vector<cudaEvent_t> events;
+  std::vector<float> times;
+  int last_launches = 0;
+  double last_bytes = 0.0;
+};
+
+namespace {
+
+int check_ctx(qaoa_ctx* c) {
+  if (!c) return fail(QAOA_E_INVALID, "null context");
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  return QAOA_OK;
+}
+
+int ensure_partials(qaoa_ctx* c, int n) {
+  if (c->partials_len >= n) return QAOA_OK;
+  if (c->partials) cudaFree(c->partials);
+  c->partials = nullptr;
+  c->partials_len = 0;
+  CUDA_TRY(cudaMalloc(&c->partials, sizeof(double) * (size_t)n));
+  c->partials_len = n;
+  return QAOA_OK;
+}
+
+int ensure_tables(qaoa_ctx* c, size_t n) {
+  if (c->d_tables_cap < n) {
+    if (c->d_tables) cudaFree(c->d_tables);
+    c->d_tables = nullptr;
+    c->d_tables_cap = 0;
+    CUDA_TRY(cudaMalloc(&c->d_tables, sizeof(double2) * n));
+    c->d_tables_cap = n;
+  }
+  if (c->h_tables_cap < n) {
+    if (c->h_tables) cudaFreeHost(c->h_tables);
+    c->h_tables = nullptr;
+    c->h_tables_cap = 0;
+    CUDA_TRY(cudaMallocHost(&c->h_tables, sizeof(double2) * n));
+    c->h_tables_cap = n;
+  }
+  return QAOA_OK;
+}
+
+std::vector<SetDesc> make_sets(int n) {
+  std::vector<SetDesc> sets;
+  SetDesc s0;
+  for (int k = 0; k < 12; ++k) s0.pos[k] = k;
+  s0.act = 0xFFFu;
+  sets.push_back(s0);
+  const int rem = n - 12;
+  if (rem <= 0) return sets;
+  const int chunks = (rem + 8) / 9;
+  int next = 12;
+  for (int ci = 0; ci < chunks; ++ci) {
+    const int m = rem / chunks + (ci < rem % chunks ? 1 : 0);
+    const int carried = 12 - m;
+    SetDesc s;
+    for (int k = 0; k < carried; ++k) s.pos[k] = k;
+    for (int k = 0; k < m; ++k) s.pos[carried + k] = next + k;
+    s.act = (0xFFFu >> carried) << carried;
+    next += m;
+    sets.push_back(s);
+  }
+  return sets;
+}
+
+std::vector<SweepPlan> make_plan(int n_sets, int p, bool exact) {
+  // flat op list: cost l, then mixer l over the sets in this level's order
+  struct Op {
+    int kind;  // 0 cost, 1 mixer
+    int level;
+    int set;
+  };
+  std::vector<Op> ops;
+  for (int l = 0; l < p; ++l) {
+    ops.push_back({0, l, -1});
+    const bool fwd = exact || (l % 2 == 0);
+    for (int i = 0; i < n_sets; ++i) ops.push_back({1, l, fwd ? i : n_sets - 1 - i});
+  }
+  std::vector<SweepPlan> plan;
+  size_t i = 0;
+  while (i < ops.size()) {
+    SweepPlan sp{-1, -1, -1, -1, -1};
+    if (ops[i].kind == 0) {
+      sp.pre_cost = ops[i].level;
+      ++i;
+    }
+    // ops[i] is a mixer op
+    sp.set = ops[i].set;
+    sp.stage1 = ops[i].level;
+    ++i;
+    if (!exact && i + 1 < ops.size() && ops[i].kind == 0 && ops[i + 1].kind == 1 &&
+        ops[i + 1].set == sp.set) {
+      sp.mid_cost = ops[i].level;
+      sp.stage2 = ops[i + 1].level;
+      i += 2;
+    }
+    plan.push_back(sp);
+  }
+  return plan;
+}
+
+void fill_graph(GraphDev& g, int n_nodes, const uint64_t* row_mask, int tot_edge, uint64_t x_hi) {
+  memset(&g, 0, sizeof(g));
+  g.n_nodes = n_nodes;
+  g.tot_edge = tot_edge;
+  g.x_hi = x_hi;
+  for (int i = 0; i < n_nodes; ++i) g.rm[i] = row_mask[i];
+  for (int i = 0; i < n_nodes; ++i) {
+    uint64_t m = row_mask[i];
+    while (m) {
+      const int j = __builtin_ctzll(m);
+      m &= m - 1;
+      g.adj[i] |= 1ull << j;
+      g.adj[j] |= 1ull << i;
+    }
+  }
+}
+
+int record_event(qaoa_ctx* c, bool timing, size_t idx) {
+  if (!timing) return QAOA_OK;
+  while (c->events.size() <= idx) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    c->events.push_back(e);
+  }
+  CUDA_TRY(cudaEventRecord(c->events[idx], c->stream));
+  return QAOA_OK;
+}
+
+int reduce_to_host(qaoa_ctx* c, int n_partials, int mode_max, double* out) {
+  CUDA_TRY(launch_sum_partials(c->partials, n_partials, c->d_scalar, mode_max, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(out, c->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return QAOA_OK;
+}
+
+int create_common(int n, int device, void* stream, void* ext, qaoa_ctx** out) {
+  if (!out) return fail(QAOA_E_INVALID, "null output pointer");
+  *out = nullptr;
+  if (n < 1) return fail(QAOA_E_INVALID, "qubit count must be at least 1");
+  if (n > 40) return fail(QAOA_E_INVALID, "local qubit count above 40 is not supported");
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) return fail(QAOA_E_CUDA, "no CUDA device available");
+  if (device < 0 || device >= count) return fail(QAOA_E_INVALID, "device index out of range");
+  CUDA_TRY(cudaSetDevice(device));
+  qaoa_ctx* c = new qaoa_ctx();
+  c->n = n;
+  c->device = device;
+  if (stream) {
+    c->stream = (cudaStream_t)stream;
+  } else {
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete c;
+      return cuda_fail(e, "cudaStreamCreate");
+    }
+    c->own_stream = true;
+  }
+  const size_t bytes = sizeof(double2) << n;
+  if (ext) {
+    c->amps = (double2*)ext;
+  } else {
+    e = cudaMalloc(&c->amps, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      qaoa_destroy(c);
+      char buf[160];
+      snprintf(buf, sizeof buf, "cannot allocate %.1f GiB of device memory for %d qubits",
+               bytes / 1073741824.0, n);
+      return fail(QAOA_E_NOMEM, buf);
+    }
+    c->own_amps = true;
+  }
+  e = cudaMalloc(&c->d_scalar, sizeof(double) * 2);
+  if (e != cudaSuccess) {
+    qaoa_destroy(c);
+    return cuda_fail(e, "cudaMalloc");
+  }
+  int rc = ensure_partials(c, reduce_grid());
+  if (rc) {
+    qaoa_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return QAOA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* qaoa_last_error(void) { return g_last_error.c_str(); }
+
+const char* qaoa_version(void) { return "qaoa_b200 0.1 sm_100a"; }
+
+int qaoa_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int qaoa_create(int n_qubits, int device, void* stream, qaoa_ctx** out) {
+  return create_common(n_qubits, device, stream, nullptr, out);
+}
+
+int qaoa_create_external(int n_qubits, int device, void* stream, void* device_amps,
+                         qaoa_ctx** out) {
+  if (!device_amps) return fail(QAOA_E_INVALID, "null device buffer");
+  return create_common(n_qubits, device, stream, device_amps, out);
+}
+
+void qaoa_destroy(qaoa_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->own_amps && c->amps) cudaFree(c->amps);
+  if (c->cut_table) cudaFree(c->cut_table);
+  if (c->partials) cudaFree(c->partials);
+  if (c->d_scalar) cudaFree(c->d_scalar);
+  if (c->d_tables) cudaFree(c->d_tables);
+  if (c->h_tables) cudaFreeHost(c->h_tables);
+  for (auto e : c->events) cudaEventDestroy(e);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+void* qaoa_state_ptr(qaoa_ctx* c) { return c ? (void*)c->amps : nullptr; }
+
+int qaoa_set_stream(qaoa_ctx* c, void* stream) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (c->own_stream && c->stream) {
+    cudaStreamSynchronize(c->stream);
+    cudaStreamDestroy(c->stream);
+  }
+  c->own_stream = false;
+  c->stream = (cudaStream_t)stream;
+  return QAOA_OK;
+}
+
+int qaoa_set_graph(qaoa_ctx* c, int n_nodes, const uint64_t* row_mask, int tot_edge,
+                   uint64_t x_hi) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (n_nodes < c->n || n_nodes > kMaxNodes)
+    return fail(QAOA_E_INVALID, "graph node count must be in [n_local, 64]");
+  if (!row_mask && n_nodes) return fail(QAOA_E_INVALID, "null row_mask");
+  if (x_hi & ((1ull << c->n) - 1ull)) return fail(QAOA_E_INVALID, "x_hi overlaps local bits");
+  int edges = 0;
+  for (int i = 0; i < n_nodes; ++i) {
+    const uint64_t m = row_mask[i];
+    if (n_nodes < 64 && (m >> n_nodes)) return fail(QAOA_E_INVALID, "row mask has bits above n");
+    if (m & ((2ull << i) - 1ull)) return fail(QAOA_E_INVALID, "row mask is not strictly upper");
+    edges += __builtin_popcountll(m);
+  }
+  if (edges != tot_edge) return fail(QAOA_E_INVALID, "tot_edge does not match the row masks");
+  fill_graph(c->g, n_nodes, row_mask, tot_edge, x_hi);
+  c->has_graph = true;
+  c->expect_valid = false;
+  if (c->cut_table) {
+    cudaFree(c->cut_table);
+    c->cut_table = nullptr;
+  }
+  return QAOA_OK;
+}
+
+int qaoa_init_uniform(qaoa_ctx* c) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  const int n_total = c->has_graph ? c->g.n_nodes : c->n;
+  const double u = sqrt(1.0 / (double)(1ull << n_total));
+  CUDA_TRY(launch_fill(c->amps, 1ull << c->n, make_double2(u, 0.0), c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->expect_valid = false;
+  return QAOA_OK;
+}
+
+int qaoa_write_amplitudes(qaoa_ctx* c, uint64_t offset, uint64_t count, const double* src) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (offset + count > (1ull << c->n) || offset + count < offset)
+    return fail(QAOA_E_RANGE, "amplitude range out of bounds");
+  if (count && !src) return fail(QAOA_E_INVALID, "null source");
+  CUDA_TRY(cudaMemcpyAsync(c->amps + offset, src, count * sizeof(double2), cudaMemcpyHostToDevice,
+                           c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->expect_valid = false;
+  return QAOA_OK;
+}
+
+int qaoa_read_amplitudes(qaoa_ctx* c, uint64_t offset, uint64_t count, double* dst) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (offset + count > (1ull << c->n) || offset + count < offset)
+    return fail(QAOA_E_RANGE, "amplitude range out of bounds");
+  if (count && !dst) return fail(QAOA_E_INVALID, "null destination");
+  CUDA_TRY(cudaMemcpyAsync(dst, c->amps + offset, count * sizeof(double2), cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return QAOA_OK;
+}
+
+int qaoa_apply_cost(qaoa_ctx* c, const double* phase_table) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (!c->has_graph) return fail(QAOA_E_STATE, "no graph set");
+  if (!phase_table) return fail(QAOA_E_INVALID, "null phase table");
+  const size_t len = 2 * (size_t)c->g.tot_edge + 1;
+  if ((rc = ensure_tables(c, len))) return rc;
+  memcpy(c->h_tables, phase_table, len * sizeof(double2));
+  CUDA_TRY(cudaMemcpyAsync(c->d_tables, c->h_tables, len * sizeof(double2),
+                           cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(launch_cost_gate(c->amps, 1ull << c->n, c->g, c->d_tables, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->expect_valid = false;
+  return QAOA_OK;
+}
+
+int qaoa_apply_rx(qaoa_ctx* c, int qubit, double cs, double sn) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (qubit < 0 || qubit >= c->n) {
+    char buf[96];
+    snprintf(buf, sizeof buf, "qubit %d out of range for n=%d", qubit, c->n);
+    return fail(QAOA_E_RANGE, buf);
+  }
+  CUDA_TRY(launch_rx_gate(c->amps, c->n, qubit, cs, sn, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->expect_valid = false;
+  return QAOA_OK;
+}
+
+static int run_exact_mixer_sweeps(qaoa_ctx* c, double cs, double sn) {
+  // all sets, RX stage only, exact arithmetic and order
+  const std::vector<SetDesc> sets = make_sets(c->n);
+  const int grid = (int)(1ll << (c->n - 12));  // one 4096-amplitude tile per CTA
+  for (const SetDesc& s : sets) {
+    SweepArgs a;
+    memset(&a, 0, sizeof(a));
+    a.amps = c->amps;
+    a.g = c->g;
+    a.ntiles = 1ll << (c->n - 12);
+    memcpy(a.pos, s.pos, sizeof(a.pos));
+    memcpy(a.ins, s.pos, sizeof(a.ins));
+    std::sort(a.ins, a.ins + 12);
+    a.act1 = s.act;
+    a.rx1 = RxStage{cs, sn, 0};
+    a.flags = kStage1 | kExact;
+    a.table_len = 0;
+    CUDA_TRY(launch_sweep(a, grid, c->stream));
+  }
+  return QAOA_OK;
+}
+
+int qaoa_apply_mixer(qaoa_ctx* c, double cs, double sn) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (c->n >= 12) {
+    if ((rc = run_exact_mixer_sweeps(c, cs, sn))) return rc;
+  } else {
+    for (int q = 0; q < c->n; ++q) CUDA_TRY(launch_rx_gate(c->amps, c->n, q, cs, sn, c->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->expect_valid = false;
+  return QAOA_OK;
+}
+
+int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double* cs,
+                    const double* sn, int flags) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (!c->has_graph) return fail(QAOA_E_STATE, "no graph set");
+  if (p < 0) return fail(QAOA_E_INVALID, "level count must be non-negative");
+  if (p > 0 && (!phase_tables || !cs || !sn)) return fail(QAOA_E_INVALID, "null angle arrays");
+  const bool exact = flags & QAOA_RUN_EXACT;
+  const bool from_state = flags & QAOA_RUN_FROM_STATE;
+  const bool want_expect = flags & QAOA_RUN_EXPECTATION;
+  const bool timing = flags & QAOA_RUN_TIMING;
+  const int n = c->n;
+  const int n_total = c->g.n_nodes;
+  const int tl = 2 * c->g.tot_edge + 1;
+  c->expect_valid = false;
+  c->last_launches = 0;
+  c->last_bytes = 0.0;
+  c->times.clear();
+  size_t ev = 0;
+  const double u = sqrt(1.0 / (double)(1ull << n_total));
+  const uint64_t size = 1ull << n;
+
+  if (n < 12) {
+    // Small states: per-gate kernels (bit-exact in both modes).
+    if ((rc = ensure_tables(c, (size_t)tl * std::max(p, 1)))) return rc;
+    memcpy(c->h_tables, phase_tables, sizeof(double2) * (size_t)tl * p);
+    CUDA_TRY(cudaMemcpyAsync(c->d_tables, c->h_tables, sizeof(double2) * (size_t)tl * p,
+                             cudaMemcpyHostToDevice, c->stream));
+    if ((rc = record_event(c, timing, ev++))) return rc;
+    if (!from_state) {
+      CUDA_TRY(launch_fill(c->amps, size, make_double2(u, 0.0), c->stream));
+      ++c->last_launches;
+    }
+    for (int l = 0; l < p; ++l) {
+      CUDA_TRY(launch_cost_gate(c->amps, size, c->g, c->d_tables + (size_t)l * tl, c->stream));
+      ++c->last_launches;
+      for (int q = 0; q < n; ++q) {
+        CUDA_TRY(launch_rx_gate(c->amps, n, q, cs[l], sn[l], c->stream));
+        ++c->last_launches;
+      }
+    }
+    if ((rc = record_event(c, timing, ev++))) return rc;
+    if (want_expect) {
+      const int grid = reduce_grid();
+      CUDA_TRY(launch_expectation(c->amps, n, c->g, c->partials, grid, c->stream));
+      ++c->last_launches;
+      if ((rc = reduce_to_host(c, grid, 0, &c->expect_value))) return rc;
+      c->expect_valid = true;
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (timing) {
+      float ms = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&ms, c->events[0], c->events[1]));
+      c->times.push_back(ms);
+    }
+    return QAOA_OK;
+  }
+
+  // ---- tiled path --------------------------------------------------------
+  const std::vector<SetDesc> sets = make_sets(n);
+  std::vector<SweepPlan> plan = make_plan((int)sets.size(), p, exact);
+
+  // phase tables: exact = as given; fast = scaled by the previous level's factor
+  std::vector<RxStage> stages(std::max(p, 1));
+  std::complex<double> prev_scale(1.0, 0.0);
+  if ((rc = ensure_tables(c, (size_t)tl * std::max(p, 1)))) return rc;
+  for (int l = 0; l < p; ++l) {
+    const std::complex<double> f_scale = prev_scale;
+    const double* src = phase_tables + (size_t)2 * tl * l;
+    for (int k = 0; k < tl; ++k) {
+      std::complex<double> v(src[2 * k], src[2 * k + 1]);
+      if (!exact) v *= f_scale;
+      c->h_tables[(size_t)l * tl + k] = make_double2(v.real(), v.imag());
+    }
+    if (exact) {
+      stages[l] = RxStage{cs[l], sn[l], 0};
+    } else if (std::fabs(cs[l]) >= std::fabs(sn[l])) {
+      stages[l] = RxStage{sn[l] / cs[l], 0.0, 1};
+      prev_scale = std::pow(std::complex<double>(cs[l], 0.0), n_total);
+    } else {
+      stages[l] = RxStage{cs[l] / sn[l], 0.0, 2};
+      prev_scale = std::pow(std::complex<double>(0.0, -sn[l]), n_total);
+    }
+  }
+  if (p > 0)
+    CUDA_TRY(cudaMemcpyAsync(c->d_tables, c->h_tables, sizeof(double2) * (size_t)tl * p,
+                             cudaMemcpyHostToDevice, c->stream));
+  const std::complex<double> final_scale = exact ? std::complex<double>(1.0, 0.0) : prev_scale;
+
+  const int64_t ntiles = 1ll << (n - 12);
+  const int grid = (int)ntiles;  // one 4096-amplitude tile per CTA
+  if (want_expect && (rc = ensure_partials(c, grid))) return rc;
+
+  if (p == 0) {
+    if (!from_state) {
+      CUDA_TRY(launch_fill(c->amps, size, make_double2(u, 0.0), c->stream));
+      ++c->last_launches;
+      c->last_bytes += 16.0 * size;
+    }
+    if (want_expect) {
+      const int g2 = reduce_grid();
+      CUDA_TRY(launch_expectation(c->amps, n, c->g, c->partials, g2, c->stream));
+      ++c->last_launches;
+      if ((rc = reduce_to_host(c, g2, 0, &c->expect_value))) return rc;
+      c->expect_valid = true;
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return QAOA_OK;
+  }
+
+  if ((rc = record_event(c, timing, ev++))) return rc;
+  for (size_t i = 0; i < plan.size(); ++i) {
+    const SweepPlan& sp = plan[i];
+    const SetDesc& s = sets[sp.set];
+    SweepArgs a;
+    memset(&a, 0, sizeof(a));
+    a.amps = c->amps;
+    a.g = c->g;
+    a.ntiles = ntiles;
+    a.partials = c->partials;
+    memcpy(a.pos, s.pos, sizeof(a.pos));
+    memcpy(a.ins, s.pos, sizeof(a.ins));
+    std::sort(a.ins, a.ins + 12);
+    uint32_t fl = exact ? kExact : 0u;
+    if (i == 0 && !from_state) {
+      fl |= kGen;
+      a.gen = make_double2(u, 0.0);
+    }
+    a.table_len = tl;
+    if (sp.pre_cost >= 0) {
+      fl |= kPreCost;
+      a.table = c->d_tables + (size_t)sp.pre_cost * tl;
+    }
+    if (sp.mid_cost >= 0) {
+      fl |= kMidCost;
+      a.table2 = c->d_tables + (size_t)sp.mid_cost * tl;
+    }
+    if (sp.stage1 >= 0) {
+      fl |= kStage1;
+      a.act1 = s.act;
+      a.rx1 = stages[sp.stage1];
+    }
+    if (sp.stage2 >= 0) {
+      fl |= kStage2;
+      a.act2 = s.act;
+      a.rx2 = stages[sp.stage2];
+    }
+    const bool last = i + 1 == plan.size();
+    if (last && !exact) {
+      fl |= kScale;
+      a.scale = make_double2(final_scale.real(), final_scale.imag());
+    }
+    if (last && want_expect) fl |= kExpect;
+    a.flags = fl;
+    CUDA_TRY(launch_sweep(a, grid, c->stream));
+    ++c->last_launches;
+    c->last_bytes += ((fl & kGen) ? 16.0 : 32.0) * (double)size;
+    if ((rc = record_event(c, timing, ev++))) return rc;
+  }
+  if (want_expect) {
+    if ((rc = reduce_to_host(c, grid, 0, &c->expect_value))) return rc;
+    ++c->last_launches;
+    c->expect_valid = true;
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (timing) {
+    for (size_t i = 0; i + 1 < ev; ++i) {
+      float ms = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&ms, c->events[i], c->events[i + 1]));
+      c->times.push_back(ms);
+    }
+  }
+  return QAOA_OK;
+}
+
+int qaoa_expectation(qaoa_ctx* c, double* out) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (!out) return fail(QAOA_E_INVALID, "null output");
+  if (!c->has_graph) return fail(QAOA_E_STATE, "no graph set");
+  if (c->expect_valid) {
+    *out = c->expect_value;
+    return QAOA_OK;
+  }
+  const int grid = reduce_grid();
+  if ((rc = ensure_partials(c, grid))) return rc;
+  CUDA_TRY(launch_expectation(c->amps, c->n, c->g, c->partials, grid, c->stream));
+  if ((rc = reduce_to_host(c, grid, 0, out))) return rc;
+  c->expect_value = *out;
+  c->expect_valid = true;
+  return QAOA_OK;
+}
+
+int qaoa_norm_sq(qaoa_ctx* c, double* out) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (!out) return fail(QAOA_E_INVALID, "null output");
+  const int grid = reduce_grid();
+  if ((rc = ensure_partials(c, grid))) return rc;
+  CUDA_TRY(launch_norm_sq(c->amps, 1ull << c->n, c->partials, grid, c->stream));
+  return reduce_to_host(c, grid, 0, out);
+}
+
+int qaoa_max_abs_diff(qaoa_ctx* a, qaoa_ctx* b, double* out) {
+  int rc = check_ctx(a);
+  if (rc) return rc;
+  if (!b || !out) return fail(QAOA_E_INVALID, "null argument");
+  if (a->n != b->n) {
+    char buf[96];
+    snprintf(buf, sizeof buf, "qubit counts differ: %d vs %d", a->n, b->n);
+    return fail(QAOA_E_INVALID, buf);
+  }
+  if (a->device != b->device) return fail(QAOA_E_INVALID, "states live on different devices");
+  CUDA_TRY(cudaStreamSynchronize(b->stream));
+  const int grid = reduce_grid();
+  if ((rc = ensure_partials(a, grid))) return rc;
+  CUDA_TRY(launch_max_abs_diff(a->amps, b->amps, 1ull << a->n, a->partials, grid, a->stream));
+  return reduce_to_host(a, grid, 1, out);
+}
+
+int qaoa_build_cut_table(qaoa_ctx* c) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (!c->has_graph) return fail(QAOA_E_STATE, "no graph set");
+  const int bytes_per = c->g.tot_edge <= 255 ? 1 : 2;
+  if (!c->cut_table || c->cut_bytes != bytes_per) {
+    if (c->cut_table) cudaFree(c->cut_table);
+    c->cut_table = nullptr;
+    cudaError_t e = cudaMalloc(&c->cut_table, (size_t)bytes_per << c->n);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(QAOA_E_NOMEM, "cannot allocate the cut table");
+    }
+    c->cut_bytes = bytes_per;
+  }
+  CUDA_TRY(launch_cut_table(c->cut_table, bytes_per, c->n, c->g, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return QAOA_OK;
+}
+
+int qaoa_read_cut_table(qaoa_ctx* c, uint64_t offset, uint64_t count, int64_t* dst) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (!c->cut_table) return fail(QAOA_E_STATE, "cut table not built");
+  if (offset + count > (1ull << c->n)) return fail(QAOA_E_RANGE, "cut-table range out of bounds");
+  if (count && !dst) return fail(QAOA_E_INVALID, "null destination");
+  std::vector<uint8_t> tmp(count * c->cut_bytes);
+  CUDA_TRY(cudaMemcpyAsync(tmp.data(), (uint8_t*)c->cut_table + offset * c->cut_bytes,
+                           count * c->cut_bytes, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (c->cut_bytes == 1) {
+    for (uint64_t i = 0; i < count; ++i) dst[i] = tmp[i];
+  } else {
+    const uint16_t* t16 = (const uint16_t*)tmp.data();
+    for (uint64_t i = 0; i < count; ++i) dst[i] = t16[i];
+  }
+  return QAOA_OK;
+}
+
+int qaoa_free_cut_table(qaoa_ctx* c) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (c->cut_table) cudaFree(c->cut_table);
+  c->cut_table = nullptr;
+  return QAOA_OK;
+}
+
+int qaoa_layer_timings(qaoa_ctx* c, float* ms, int cap) {
+  if (!c) return fail(QAOA_E_INVALID, "null context");
+  const int n = (int)c->times.size();
+  for (int i = 0; i < n && i < cap; ++i) ms[i] = c->times[i];
+  return n;
+}
+
+int qaoa_last_run_stats(qaoa_ctx* c, int* launches, double* hbm_bytes) {
+  if (!c) return fail(QAOA_E_INVALID, "null context");
+  if (launches) *launches = c->last_launches;
+  if (hbm_bytes) *hbm_bytes = c->last_bytes;
+  return QAOA_OK;
+}
+
+int qaoa_synchronize(qaoa_ctx* c) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return QAOA_OK;
+}
+
+int qaoa_pack_chunks(qaoa_ctx* c, int g, const int* local_bits, void* dst) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (g < 0 || g > 8 || g > c->n || (g && (!local_bits || !dst)))
+    return fail(QAOA_E_INVALID, "bad chunk spec");
+  for (int k = 0; k < g; ++k) {
+    if (local_bits[k] < 0 || local_bits[k] >= c->n || (k && local_bits[k] <= local_bits[k - 1]))
+      return fail(QAOA_E_INVALID, "local bits must be ascending and in range");
+  }
+  CUDA_TRY(launch_pack_chunks(c->amps, c->n, g, local_bits, (double2*)dst, c->stream));
+  return QAOA_OK;
+}
+
+int qaoa_unpack_chunks(qaoa_ctx* c, int g, const int* local_bits, const void* src) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (g < 0 || g > 8 || g > c->n || (g && (!local_bits || !src)))
+    return fail(QAOA_E_INVALID, "bad chunk spec");
+  for (int k = 0; k < g; ++k) {
+    if (local_bits[k] < 0 || local_bits[k] >= c->n || (k && local_bits[k] <= local_bits[k - 1]))
+      return fail(QAOA_E_INVALID, "local bits must be ascending and in range");
+  }
+  CUDA_TRY(launch_unpack_chunks(c->amps, c->n, g, local_bits, (const double2*)src, c->stream));
+  c->expect_valid = false;
+  return QAOA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,350 @@
+// qaoa_gates.cu -- per-gate and per-element kernels of the B200 QAOA engine:
+// single cost layer, single-qubit RX, launch-control fill, <C> reduction, norm,
+// max-abs-diff, the bitwise cut-table builder and the shard pack/unpack used by
+// the global-qubit exchange.  The fused multi-qubit sweeps are in qaoa_sweep.cu.
+#include "qaoa_common.cuh"
+#include "qaoa_sweep.h"
+
+namespace qb {
+
+constexpr int kBlock = 256;
+
+static int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms < 1) sms = 1;
+  }
+  return sms;
+}
+
+int reduce_grid() { return num_sms() * 4; }
+
+static int grid_for(uint64_t work, int per_thread) {
+  const uint64_t threads = (work + per_thread - 1) / per_thread;
+  uint64_t blocks = (threads + kBlock - 1) / kBlock;
+  const uint64_t cap = (uint64_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+// ---- launch control: circuit.py:42-48 -------------------------------------
+__global__ void fill_kernel(double2* __restrict__ amps, uint64_t n, double2 v) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    __stcs(amps + i, v);
+}
+
+cudaError_t launch_fill(double2* amps, uint64_t n, double2 v, cudaStream_t s) {
+  fill_kernel<<<grid_for(n, 4), kBlock, 0, s>>>(amps, n, v);
+  return cudaGetLastError();
+}
+
+// ---- single cost layer: apply_cost_bitwise cost.py:162-176 -----------------
+// Thread handles 16 amplitudes whose bits 5..8 vary (lanes on bits 0..4, so
+// every load instruction of a warp reads 512 contiguous bytes).
+template <bool WIDE>
+__global__ void cost_gate_kernel(double2* __restrict__ amps, int n_local, GraphDev g,
+                                 const double2* __restrict__ table) {
+  const uint64_t groups = 1ull << (n_local - 9);   // groups of 512 amplitudes
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const int v[4] = {5, 6, 7, 8};
+  for (uint64_t w = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < groups;
+       w += warps) {
+    const uint64_t x0 = (w << 9) | (uint64_t)lane;
+    int c[16];
+    cut_counts16<WIDE>(g.x_hi | x0, v, g, c);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const uint64_t x = x0 | ((uint64_t)r << 5);
+      amps[x] = cmul_np(amps[x], table[2 * g.tot_edge - 2 * c[r]]);
+    }
+  }
+}
+
+template <bool WIDE>
+__global__ void cost_gate_small_kernel(double2* __restrict__ amps, uint64_t n, GraphDev g,
+                                       const double2* __restrict__ table) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const int c = cut_count<WIDE>(g.x_hi | x, g);
+    amps[x] = cmul_np(amps[x], table[2 * g.tot_edge - 2 * c]);
+  }
+}
+
+cudaError_t launch_cost_gate(double2* amps, uint64_t n, const GraphDev& g, const double2* table,
+                             cudaStream_t s) {
+  int n_local = 0;
+  while ((1ull << n_local) < n) ++n_local;
+  const bool wide = g.n_nodes > 32;
+  if (n_local >= 9) {
+    const int grid = grid_for(n, 16);
+    if (wide) cost_gate_kernel<true><<<grid, kBlock, 0, s>>>(amps, n_local, g, table);
+    else cost_gate_kernel<false><<<grid, kBlock, 0, s>>>(amps, n_local, g, table);
+  } else {
+    if (wide) cost_gate_small_kernel<true><<<1, kBlock, 0, s>>>(amps, n, g, table);
+    else cost_gate_small_kernel<false><<<1, kBlock, 0, s>>>(amps, n, g, table);
+  }
+  return cudaGetLastError();
+}
+
+// ---- single-qubit RX: apply_rx state.py:110-128 (bit-exact) ----------------
+__global__ void rx_gate_kernel(double2* __restrict__ amps, int n_local, int q, double c,
+                               double sn) {
+  const uint64_t half = 1ull << (n_local - 1);
+  const uint64_t stride = 1ull << q;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < half;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = ((k >> q) << (q + 1)) | (k & (stride - 1));
+    double2 a = amps[i0], b = amps[i0 | stride];
+    rx_exact(a, b, c, sn);
+    amps[i0] = a;
+    amps[i0 | stride] = b;
+  }
+}
+
+cudaError_t launch_rx_gate(double2* amps, int n_local, int q, double c, double sn,
+                           cudaStream_t s) {
+  rx_gate_kernel<<<grid_for(1ull << (n_local - 1), 2), kBlock, 0, s>>>(amps, n_local, q, c, sn);
+  return cudaGetLastError();
+}
+
+// ---- <C> reduction: expectation circuit.py:116-121 -------------------------
+template <bool WIDE>
+__global__ void expectation_kernel(const double2* __restrict__ amps, int n_local, GraphDev g,
+                                   double* __restrict__ partials) {
+  __shared__ double scratch[kBlock / 32];
+  double acc = 0.0;
+  if (n_local >= 9) {
+    const uint64_t groups = 1ull << (n_local - 9);
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const int v[4] = {5, 6, 7, 8};
+    for (uint64_t w = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < groups;
+         w += warps) {
+      const uint64_t x0 = (w << 9) | (uint64_t)lane;
+      int c[16];
+      cut_counts16<WIDE>(g.x_hi | x0, v, g, c);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const double2 a = __ldcs(amps + (x0 | ((uint64_t)r << 5)));
+        acc += (a.x * a.x + a.y * a.y) * (double)c[r];
+      }
+    }
+  } else {
+    const uint64_t n = 1ull << n_local;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+      const double2 a = amps[x];
+      acc += (a.x * a.x + a.y * a.y) * (double)cut_count<WIDE>(g.x_hi | x, g);
+    }
+  }
+  const double t = block_sum<kBlock>(acc, scratch);
+  if (threadIdx.x == 0) partials[blockIdx.x] = t;
+}
+
+cudaError_t launch_expectation(const double2* amps, int n_local, const GraphDev& g,
+                               double* partials, int grid, cudaStream_t s) {
+  if (g.n_nodes > 32) expectation_kernel<true><<<grid, kBlock, 0, s>>>(amps, n_local, g, partials);
+  else expectation_kernel<false><<<grid, kBlock, 0, s>>>(amps, n_local, g, partials);
+  return cudaGetLastError();
+}
+
+// ---- norm^2 and max |a - b| (state.py:50-51, :152-156) ---------------------
+__global__ void norm_sq_kernel(const double2* __restrict__ amps, uint64_t n,
+                               double* __restrict__ partials) {
+  __shared__ double scratch[kBlock / 32];
+  double acc = 0.0;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const double2 a = __ldcs(amps + x);
+    acc += a.x * a.x + a.y * a.y;
+  }
+  const double t = block_sum<kBlock>(acc, scratch);
+  if (threadIdx.x == 0) partials[blockIdx.x] = t;
+}
+
+cudaError_t launch_norm_sq(const double2* amps, uint64_t n, double* partials, int grid,
+                           cudaStream_t s) {
+  norm_sq_kernel<<<grid, kBlock, 0, s>>>(amps, n, partials);
+  return cudaGetLastError();
+}
+
+__global__ void max_abs_diff_kernel(const double2* __restrict__ a, const double2* __restrict__ b,
+                                    uint64_t n, double* __restrict__ partials) {
+  __shared__ double scratch[kBlock / 32];
+  double m = 0.0;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const double2 u = a[x], v = b[x];
+    m = fmax(m, hypot(u.x - v.x, u.y - v.y));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kBlock / 32; ++w) t = fmax(t, scratch[w]);
+    partials[blockIdx.x] = t;
+  }
+}
+
+cudaError_t launch_max_abs_diff(const double2* a, const double2* b, uint64_t n, double* partials,
+                                int grid, cudaStream_t s) {
+  max_abs_diff_kernel<<<grid, kBlock, 0, s>>>(a, b, n, partials);
+  return cudaGetLastError();
+}
+
+// Fixed-order pairwise reduction of the block partials (deterministic).
+__global__ void sum_partials_kernel(const double* __restrict__ partials, int n,
+                                    double* __restrict__ out, int mode_max) {
+  __shared__ double s[1024];
+  double v = mode_max ? 0.0 : 0.0;
+  // thread t folds partials t, t+1024, ... in order
+  for (int i = threadIdx.x; i < n; i += 1024) v = mode_max ? fmax(v, partials[i]) : v + partials[i];
+  s[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      s[threadIdx.x] = mode_max ? fmax(s[threadIdx.x], s[threadIdx.x + w])
+                                : s[threadIdx.x] + s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
+}
+
+cudaError_t launch_sum_partials(const double* partials, int n, double* out, int mode_max,
+                                cudaStream_t s) {
+  sum_partials_kernel<<<1, 1024, 0, s>>>(partials, n, out, mode_max);
+  return cudaGetLastError();
+}
+
+// ---- cut-table builder: CompressedCostPlan.cut_counts cost.py:88-99 --------
+// Thread t writes C(x) for x = 16t .. 16t+15 as one 16-byte (uint8) or two
+// 16-byte (uint16) stores: C(16t) from the row-mask popcount sweep, the other
+// 15 by flipping nodes 0..3 (delta = deg - 2 popc(adj & x), -2 per flipped edge).
+template <bool WIDE, typename T>
+__global__ void cut_table_kernel(T* __restrict__ table, int n_local, GraphDev g) {
+  const uint64_t groups = 1ull << (n_local - 4);
+  const int v[4] = {0, 1, 2, 3};
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < groups;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    int c[16];
+    cut_counts16<WIDE>(g.x_hi | (t << 4), v, g, c);
+    if (sizeof(T) == 1) {
+      uint4 o;
+      o.x = (uint32_t)c[0] | ((uint32_t)c[1] << 8) | ((uint32_t)c[2] << 16) | ((uint32_t)c[3] << 24);
+      o.y = (uint32_t)c[4] | ((uint32_t)c[5] << 8) | ((uint32_t)c[6] << 16) | ((uint32_t)c[7] << 24);
+      o.z = (uint32_t)c[8] | ((uint32_t)c[9] << 8) | ((uint32_t)c[10] << 16) | ((uint32_t)c[11] << 24);
+      o.w = (uint32_t)c[12] | ((uint32_t)c[13] << 8) | ((uint32_t)c[14] << 16) | ((uint32_t)c[15] << 24);
+      __stcs(reinterpret_cast<uint4*>(table) + t, o);
+    } else {
+      uint4 o0, o1;
+      o0.x = (uint32_t)c[0] | ((uint32_t)c[1] << 16);
+      o0.y = (uint32_t)c[2] | ((uint32_t)c[3] << 16);
+      o0.z = (uint32_t)c[4] | ((uint32_t)c[5] << 16);
+      o0.w = (uint32_t)c[6] | ((uint32_t)c[7] << 16);
+      o1.x = (uint32_t)c[8] | ((uint32_t)c[9] << 16);
+      o1.y = (uint32_t)c[10] | ((uint32_t)c[11] << 16);
+      o1.z = (uint32_t)c[12] | ((uint32_t)c[13] << 16);
+      o1.w = (uint32_t)c[14] | ((uint32_t)c[15] << 16);
+      __stcs(reinterpret_cast<uint4*>(table) + 2 * t, o0);
+      __stcs(reinterpret_cast<uint4*>(table) + 2 * t + 1, o1);
+    }
+  }
+}
+
+template <bool WIDE, typename T>
+__global__ void cut_table_small_kernel(T* __restrict__ table, uint64_t n, GraphDev g) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n;
+       x += (uint64_t)gridDim.x * blockDim.x)
+    table[x] = (T)cut_count<WIDE>(g.x_hi | x, g);
+}
+
+cudaError_t launch_cut_table(void* table, int bytes_per, int n_local, const GraphDev& g,
+                             cudaStream_t s) {
+  const bool wide = g.n_nodes > 32;
+  const uint64_t n = 1ull << n_local;
+  if (n_local >= 4) {
+    const int grid = grid_for(n, 16);
+    if (bytes_per == 1) {
+      if (wide) cut_table_kernel<true, uint8_t><<<grid, kBlock, 0, s>>>((uint8_t*)table, n_local, g);
+      else cut_table_kernel<false, uint8_t><<<grid, kBlock, 0, s>>>((uint8_t*)table, n_local, g);
+    } else {
+      if (wide) cut_table_kernel<true, uint16_t><<<grid, kBlock, 0, s>>>((uint16_t*)table, n_local, g);
+      else cut_table_kernel<false, uint16_t><<<grid, kBlock, 0, s>>>((uint16_t*)table, n_local, g);
+    }
+  } else {
+    if (bytes_per == 1) {
+      if (wide) cut_table_small_kernel<true, uint8_t><<<1, kBlock, 0, s>>>((uint8_t*)table, n, g);
+      else cut_table_small_kernel<false, uint8_t><<<1, kBlock, 0, s>>>((uint8_t*)table, n, g);
+    } else {
+      if (wide) cut_table_small_kernel<true, uint16_t><<<1, kBlock, 0, s>>>((uint16_t*)table, n, g);
+      else cut_table_small_kernel<false, uint16_t><<<1, kBlock, 0, s>>>((uint16_t*)table, n, g);
+    }
+  }
+  return cudaGetLastError();
+}
+
+// ---- shard pack / unpack for the global-qubit exchange ---------------------
+// Chunk d (d in [0, 2^g)) = the amplitudes whose local bits L[0..g-1] spell d,
+// ordered by their remaining local bits.  pack gathers, unpack scatters.
+struct BitList {
+  int b[8];
+  int g;
+};
+
+__device__ __forceinline__ uint64_t chunk_index(uint64_t i, uint64_t d, const BitList& L) {
+  // insert zeros at the sorted positions L.b (ascending), then set bits of d
+  uint64_t x = i;
+  for (int k = 0; k < L.g; ++k) {
+    const int p = L.b[k];
+    x = ((x >> p) << (p + 1)) | (x & ((1ull << p) - 1ull));
+  }
+  for (int k = 0; k < L.g; ++k) x |= ((d >> k) & 1ull) << L.b[k];
+  return x;
+}
+
+template <bool PACK>
+__global__ void chunk_kernel(double2* __restrict__ amps, int n_local, BitList L,
+                             double2* __restrict__ buf) {
+  const uint64_t chunk = 1ull << (n_local - L.g);
+  const uint64_t total = 1ull << n_local;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < total;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t d = j / chunk, i = j % chunk;
+    const uint64_t x = chunk_index(i, d, L);
+    if (PACK) buf[j] = amps[x];
+    else amps[x] = buf[j];
+  }
+}
+
+static BitList make_bits(int g, const int* local_bits) {
+  BitList L;
+  L.g = g;
+  for (int k = 0; k < g; ++k) L.b[k] = local_bits[k];
+  return L;
+}
+
+cudaError_t launch_pack_chunks(const double2* amps, int n_local, int g, const int* local_bits,
+                               double2* dst, cudaStream_t s) {
+  BitList L = make_bits(g, local_bits);
+  chunk_kernel<true><<<grid_for(1ull << n_local, 4), kBlock, 0, s>>>(const_cast<double2*>(amps),
+                                                                       n_local, L, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_chunks(double2* amps, int n_local, int g, const int* local_bits,
+                                 const double2* src, cudaStream_t s) {
+  BitList L = make_bits(g, local_bits);
+  chunk_kernel<false><<<grid_for(1ull << n_local, 4), kBlock, 0, s>>>(amps, n_local, L,
+                                                                        const_cast<double2*>(src));
+  return cudaGetLastError();
+}
+
+}  // namespace qb

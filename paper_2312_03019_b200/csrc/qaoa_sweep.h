@@ -1,0 +1,65 @@
+// qaoa_sweep.h -- host-visible description of one fused sweep launch.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "qaoa_common.cuh"
+
+namespace qb {
+
+enum SweepFlags : uint32_t {
+  kGen = 1u << 0,      // no load: every amplitude starts as `gen` (launch control)
+  kPreCost = 1u << 1,  // cost phase before the first RX stage
+  kStage1 = 1u << 2,   // RX stage 1 on tile bits act1
+  kMidCost = 1u << 3,  // cost phase between the two RX stages (fast mode)
+  kStage2 = 1u << 4,   // RX stage 2 on tile bits act2 (next level, fast mode)
+  kExpect = 1u << 5,   // accumulate sum |a|^2 C(x) into partials[blockIdx.x]
+  kScale = 1u << 6,    // multiply by `scale` before storing (fast mode)
+  kExact = 1u << 7,    // reference arithmetic + increasing qubit order
+  kNoStore = 1u << 8,  // read-only sweep
+};
+
+struct SweepArgs {
+  double2* amps;
+  const double2* table;  // phase table (2E+1) of the pre-stage cost step
+  const double2* table2; // phase table (2E+1) of the mid cost step
+  double* partials;      // [grid] block partial sums (kExpect)
+  GraphDev g;
+  int64_t ntiles;        // 2^(n_local - 12)
+  int pos[12];           // physical bit of tile bit k (pos[0..2] = 0,1,2)
+  int ins[12];           // the same positions sorted ascending (tile-number deposit)
+  unsigned act1, act2;   // active tile bits of the two RX stages
+  RxStage rx1, rx2;
+  double2 gen;
+  double2 scale;
+  int table_len;
+  uint32_t flags;
+};
+
+size_t sweep_smem_bytes(int table_len);
+cudaError_t launch_sweep(const SweepArgs& args, int grid, cudaStream_t stream);
+int sweep_max_grid(int table_len);
+
+// simple (per-gate / per-element) kernels, qaoa_gates.cu
+cudaError_t launch_fill(double2* amps, uint64_t n, double2 v, cudaStream_t s);
+cudaError_t launch_cost_gate(double2* amps, uint64_t n, const GraphDev& g, const double2* table,
+                             cudaStream_t s);
+cudaError_t launch_rx_gate(double2* amps, int n_local, int q, double c, double sn,
+                           cudaStream_t s);
+cudaError_t launch_expectation(const double2* amps, int n_local, const GraphDev& g,
+                               double* partials, int grid, cudaStream_t s);
+cudaError_t launch_norm_sq(const double2* amps, uint64_t n, double* partials, int grid,
+                           cudaStream_t s);
+cudaError_t launch_max_abs_diff(const double2* a, const double2* b, uint64_t n, double* partials,
+                                int grid, cudaStream_t s);
+cudaError_t launch_sum_partials(const double* partials, int n, double* out, int mode_max,
+                                cudaStream_t s);
+cudaError_t launch_cut_table(void* table, int bytes_per, int n_local, const GraphDev& g,
+                             cudaStream_t s);
+cudaError_t launch_pack_chunks(const double2* amps, int n_local, int g, const int* local_bits,
+                               double2* dst, cudaStream_t s);
+cudaError_t launch_unpack_chunks(double2* amps, int n_local, int g, const int* local_bits,
+                                 const double2* src, cudaStream_t s);
+int reduce_grid();
+
+}  // namespace qb
