@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -49,9 +50,11 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (_e != cudaSuccess) return cuda_fail(_e, #expr);  \
   } while (0)
 
+// One qubit set = one tile geometry: carry C (physical bits 0..C-1 ride along
+// in every tile) and the mixed range q..q+11-C (or all of 0..11 when C = 12).
 struct SetDesc {
-  int pos[12];
-  unsigned act;
+  int carry;
+  int q;
 };
 
 struct SweepPlan {
@@ -82,6 +85,10 @@ struct qaoa_ctx {
   size_t d_tables_cap = 0;  // in double2
   double2* h_tables = nullptr;  // pinned staging
   size_t h_tables_cap = 0;
+  // fast runs apply form-2 levels as form 1 + a global bit complement (X on
+  // every qubit commutes with the cost diagonal, C(~x) = C(x), and with RX):
+  // when set, the true amplitude of index x is stored at ~x.
+  bool complemented = false;
   // expectation cached from the last fused run
   bool expect_valid = false;
   double expect_value = 0.0;
@@ -131,23 +138,15 @@ int ensure_tables(qaoa_ctx* c, size_t n) {
 
 std::vector<SetDesc> make_sets(int n) {
   std::vector<SetDesc> sets;
-  SetDesc s0;
-  for (int k = 0; k < 12; ++k) s0.pos[k] = k;
-  s0.act = 0xFFFu;
-  sets.push_back(s0);
+  sets.push_back(SetDesc{12, 0});
   const int rem = n - 12;
   if (rem <= 0) return sets;
-  const int chunks = (rem + 8) / 9;
+  const int chunks = (rem + 8) / 9;  // at most 9 mixed bits per high sweep (C >= 3)
   int next = 12;
   for (int ci = 0; ci < chunks; ++ci) {
     const int m = rem / chunks + (ci < rem % chunks ? 1 : 0);
-    const int carried = 12 - m;
-    SetDesc s;
-    for (int k = 0; k < carried; ++k) s.pos[k] = k;
-    for (int k = 0; k < m; ++k) s.pos[carried + k] = next + k;
-    s.act = (0xFFFu >> carried) << carried;
+    sets.push_back(SetDesc{12 - m, next});
     next += m;
-    sets.push_back(s);
   }
   return sets;
 }
@@ -160,10 +159,21 @@ std::vector<SweepPlan> make_plan(int n_sets, int p, bool exact) {
     int set;
   };
   std::vector<Op> ops;
+  // fast mode: the low set (index 0, the only one whose merged form needs four
+  // exchanges) sits in the middle of the level order when there are >= 3 sets,
+  // so the merged level-boundary sweeps are always high sets.
+  std::vector<int> order;
+  if (!exact && n_sets >= 3) {
+    order.push_back(1);
+    order.push_back(0);
+    for (int i = 2; i < n_sets; ++i) order.push_back(i);
+  } else {
+    for (int i = 0; i < n_sets; ++i) order.push_back(i);
+  }
   for (int l = 0; l < p; ++l) {
     ops.push_back({0, l, -1});
     const bool fwd = exact || (l % 2 == 0);
-    for (int i = 0; i < n_sets; ++i) ops.push_back({1, l, fwd ? i : n_sets - 1 - i});
+    for (int i = 0; i < n_sets; ++i) ops.push_back({1, l, fwd ? order[i] : order[n_sets - 1 - i]});
   }
   std::vector<SweepPlan> plan;
   size_t i = 0;
@@ -365,17 +375,28 @@ int qaoa_init_uniform(qaoa_ctx* c) {
   CUDA_TRY(launch_fill(c->amps, 1ull << c->n, make_double2(u, 0.0), c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   c->expect_valid = false;
+  c->complemented = false;
   return QAOA_OK;
 }
 
 int qaoa_write_amplitudes(qaoa_ctx* c, uint64_t offset, uint64_t count, const double* src) {
   int rc = check_ctx(c);
   if (rc) return rc;
-  if (offset + count > (1ull << c->n) || offset + count < offset)
+  const uint64_t size = 1ull << c->n;
+  if (offset + count > size || offset + count < offset)
     return fail(QAOA_E_RANGE, "amplitude range out of bounds");
   if (count && !src) return fail(QAOA_E_INVALID, "null source");
-  CUDA_TRY(cudaMemcpyAsync(c->amps + offset, src, count * sizeof(double2), cudaMemcpyHostToDevice,
-                           c->stream));
+  if (!c->complemented) {
+    CUDA_TRY(cudaMemcpyAsync(c->amps + offset, src, count * sizeof(double2),
+                             cudaMemcpyHostToDevice, c->stream));
+  } else {  // true index x lives at ~x: reverse the chunk
+    std::vector<double2> tmp(count);
+    const double2* s2 = (const double2*)src;
+    for (uint64_t i = 0; i < count; ++i) tmp[count - 1 - i] = s2[i];
+    CUDA_TRY(cudaMemcpyAsync(c->amps + (size - offset - count), tmp.data(), count * sizeof(double2),
+                             cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   c->expect_valid = false;
   return QAOA_OK;
@@ -384,12 +405,15 @@ int qaoa_write_amplitudes(qaoa_ctx* c, uint64_t offset, uint64_t count, const do
 int qaoa_read_amplitudes(qaoa_ctx* c, uint64_t offset, uint64_t count, double* dst) {
   int rc = check_ctx(c);
   if (rc) return rc;
-  if (offset + count > (1ull << c->n) || offset + count < offset)
+  const uint64_t size = 1ull << c->n;
+  if (offset + count > size || offset + count < offset)
     return fail(QAOA_E_RANGE, "amplitude range out of bounds");
   if (count && !dst) return fail(QAOA_E_INVALID, "null destination");
-  CUDA_TRY(cudaMemcpyAsync(dst, c->amps + offset, count * sizeof(double2), cudaMemcpyDeviceToHost,
+  const uint64_t src_off = c->complemented ? size - offset - count : offset;
+  CUDA_TRY(cudaMemcpyAsync(dst, c->amps + src_off, count * sizeof(double2), cudaMemcpyDeviceToHost,
                            c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (c->complemented) std::reverse((double2*)dst, (double2*)dst + count);
   return QAOA_OK;
 }
 
@@ -426,17 +450,15 @@ int qaoa_apply_rx(qaoa_ctx* c, int qubit, double cs, double sn) {
 static int run_exact_mixer_sweeps(qaoa_ctx* c, double cs, double sn) {
   // all sets, RX stage only, exact arithmetic and order
   const std::vector<SetDesc> sets = make_sets(c->n);
-  const int grid = (int)(1ll << (c->n - 12));  // one 4096-amplitude tile per CTA
+  const int grid = (int)(1ll << (c->n - 12));  // one tile per CTA
   for (const SetDesc& s : sets) {
     SweepArgs a;
     memset(&a, 0, sizeof(a));
     a.amps = c->amps;
     a.g = c->g;
     a.ntiles = 1ll << (c->n - 12);
-    memcpy(a.pos, s.pos, sizeof(a.pos));
-    memcpy(a.ins, s.pos, sizeof(a.ins));
-    std::sort(a.ins, a.ins + 12);
-    a.act1 = s.act;
+    a.carry = s.carry;
+    a.q = s.q;
     a.rx1 = RxStage{cs, sn, 0};
     a.flags = kStage1 | kExact;
     a.table_len = 0;
@@ -490,6 +512,7 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
     if (!from_state) {
       CUDA_TRY(launch_fill(c->amps, size, make_double2(u, 0.0), c->stream));
       ++c->last_launches;
+      c->complemented = false;
     }
     for (int l = 0; l < p; ++l) {
       CUDA_TRY(launch_cost_gate(c->amps, size, c->g, c->d_tables + (size_t)l * tl, c->stream));
@@ -520,39 +543,48 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
   const std::vector<SetDesc> sets = make_sets(n);
   std::vector<SweepPlan> plan = make_plan((int)sets.size(), p, exact);
 
-  // phase tables: exact = as given; fast = scaled by the previous level's factor
+  // phase tables: the sweeps only index even entries (t = E - 2C), so upload
+  // table_even[k] = table[2k], k = 0..E.  exact = as given; fast = scaled by
+  // the previous level's factor.
+  const int te = c->g.tot_edge + 1;
   std::vector<RxStage> stages(std::max(p, 1));
   std::complex<double> prev_scale(1.0, 0.0);
-  if ((rc = ensure_tables(c, (size_t)tl * std::max(p, 1)))) return rc;
+  int flips = 0;
+  if ((rc = ensure_tables(c, (size_t)te * std::max(p, 1)))) return rc;
   for (int l = 0; l < p; ++l) {
     const std::complex<double> f_scale = prev_scale;
     const double* src = phase_tables + (size_t)2 * tl * l;
-    for (int k = 0; k < tl; ++k) {
-      std::complex<double> v(src[2 * k], src[2 * k + 1]);
+    for (int k = 0; k < te; ++k) {
+      std::complex<double> v(src[4 * k], src[4 * k + 1]);
       if (!exact) v *= f_scale;
-      c->h_tables[(size_t)l * tl + k] = make_double2(v.real(), v.imag());
+      c->h_tables[(size_t)l * te + k] = make_double2(v.real(), v.imag());
     }
     if (exact) {
       stages[l] = RxStage{cs[l], sn[l], 0};
     } else if (std::fabs(cs[l]) >= std::fabs(sn[l])) {
+      // RX = c [[1, -i t], [-i t, 1]], t = s / c
       stages[l] = RxStage{sn[l] / cs[l], 0.0, 1};
       prev_scale = std::pow(std::complex<double>(cs[l], 0.0), n_total);
     } else {
-      stages[l] = RxStage{cs[l] / sn[l], 0.0, 2};
+      // RX = (-i s) X [[1, i k], [i k, 1]], k = c / s: run form 1 with t = -k and
+      // complement every bit (X^n) by bookkeeping instead of data movement.
+      stages[l] = RxStage{-cs[l] / sn[l], 0.0, 1};
       prev_scale = std::pow(std::complex<double>(0.0, -sn[l]), n_total);
+      flips ^= 1;
     }
   }
   if (p > 0)
-    CUDA_TRY(cudaMemcpyAsync(c->d_tables, c->h_tables, sizeof(double2) * (size_t)tl * p,
+    CUDA_TRY(cudaMemcpyAsync(c->d_tables, c->h_tables, sizeof(double2) * (size_t)te * p,
                              cudaMemcpyHostToDevice, c->stream));
   const std::complex<double> final_scale = exact ? std::complex<double>(1.0, 0.0) : prev_scale;
 
   const int64_t ntiles = 1ll << (n - 12);
-  const int grid = (int)ntiles;  // one 4096-amplitude tile per CTA
+  const int grid = (int)ntiles;  // one tile per CTA (see sweep_kernel)
   if (want_expect && (rc = ensure_partials(c, grid))) return rc;
 
   if (p == 0) {
     if (!from_state) {
+      c->complemented = false;
       CUDA_TRY(launch_fill(c->amps, size, make_double2(u, 0.0), c->stream));
       ++c->last_launches;
       c->last_bytes += 16.0 * size;
@@ -578,31 +610,28 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
     a.g = c->g;
     a.ntiles = ntiles;
     a.partials = c->partials;
-    memcpy(a.pos, s.pos, sizeof(a.pos));
-    memcpy(a.ins, s.pos, sizeof(a.ins));
-    std::sort(a.ins, a.ins + 12);
+    a.carry = s.carry;
+    a.q = s.q;
     uint32_t fl = exact ? kExact : 0u;
     if (i == 0 && !from_state) {
       fl |= kGen;
       a.gen = make_double2(u, 0.0);
     }
-    a.table_len = tl;
+    a.table_len = te;
     if (sp.pre_cost >= 0) {
       fl |= kPreCost;
-      a.table = c->d_tables + (size_t)sp.pre_cost * tl;
+      a.table = c->d_tables + (size_t)sp.pre_cost * te;
     }
     if (sp.mid_cost >= 0) {
       fl |= kMidCost;
-      a.table2 = c->d_tables + (size_t)sp.mid_cost * tl;
+      a.table2 = c->d_tables + (size_t)sp.mid_cost * te;
     }
     if (sp.stage1 >= 0) {
       fl |= kStage1;
-      a.act1 = s.act;
       a.rx1 = stages[sp.stage1];
     }
     if (sp.stage2 >= 0) {
       fl |= kStage2;
-      a.act2 = s.act;
       a.rx2 = stages[sp.stage2];
     }
     const bool last = i + 1 == plan.size();
@@ -617,6 +646,7 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
     c->last_bytes += ((fl & kGen) ? 16.0 : 32.0) * (double)size;
     if ((rc = record_event(c, timing, ev++))) return rc;
   }
+  c->complemented = (from_state ? c->complemented : false) ^ (flips != 0);
   if (want_expect) {
     if ((rc = reduce_to_host(c, grid, 0, &c->expect_value))) return rc;
     ++c->last_launches;
@@ -674,7 +704,8 @@ int qaoa_max_abs_diff(qaoa_ctx* a, qaoa_ctx* b, double* out) {
   CUDA_TRY(cudaStreamSynchronize(b->stream));
   const int grid = reduce_grid();
   if ((rc = ensure_partials(a, grid))) return rc;
-  CUDA_TRY(launch_max_abs_diff(a->amps, b->amps, 1ull << a->n, a->partials, grid, a->stream));
+  const uint64_t xmask = (a->complemented != b->complemented) ? (1ull << a->n) - 1ull : 0ull;
+  CUDA_TRY(launch_max_abs_diff(a->amps, b->amps, 1ull << a->n, xmask, a->partials, grid, a->stream));
   return reduce_to_host(a, grid, 1, out);
 }
 

@@ -175,12 +175,12 @@ cudaError_t launch_norm_sq(const double2* amps, uint64_t n, double* partials, in
 }
 
 __global__ void max_abs_diff_kernel(const double2* __restrict__ a, const double2* __restrict__ b,
-                                    uint64_t n, double* __restrict__ partials) {
+                                    uint64_t n, uint64_t xmask, double* __restrict__ partials) {
   __shared__ double scratch[kBlock / 32];
   double m = 0.0;
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n;
        x += (uint64_t)gridDim.x * blockDim.x) {
-    const double2 u = a[x], v = b[x];
+    const double2 u = a[x], v = b[x ^ xmask];
     m = fmax(m, hypot(u.x - v.x, u.y - v.y));
   }
 #pragma unroll
@@ -194,9 +194,9 @@ __global__ void max_abs_diff_kernel(const double2* __restrict__ a, const double2
   }
 }
 
-cudaError_t launch_max_abs_diff(const double2* a, const double2* b, uint64_t n, double* partials,
-                                int grid, cudaStream_t s) {
-  max_abs_diff_kernel<<<grid, kBlock, 0, s>>>(a, b, n, partials);
+cudaError_t launch_max_abs_diff(const double2* a, const double2* b, uint64_t n, uint64_t xmask,
+                                double* partials, int grid, cudaStream_t s) {
+  max_abs_diff_kernel<<<grid, kBlock, 0, s>>>(a, b, n, xmask, partials);
   return cudaGetLastError();
 }
 

@@ -1,18 +1,24 @@
 // qaoa_sweep.cu -- the fused cost + mixer sweep kernel (the hot path).
 //
-// One launch = one HBM round trip of the state.  The state is cut into tiles of
-// 2^12 amplitudes (64 KiB) whose 12 "tile bits" sit at arbitrary physical bit
-// positions pos[0..11] (pos[0..2] = 0, 1, 2 always, so every HBM access is a
-// run of >= 8 consecutive amplitudes = 128 B).  A CTA of 256 threads holds the
-// tile in registers, 16 amplitudes per thread, and re-maps it through shared
-// memory between three register groups of 4 tile bits:
-//   M2: registers = tile bits 8..11, threads = tile bits 0..7  (coalesced load)
+// One launch = one HBM round trip of the state (read 16 B + write 16 B per
+// amplitude; launch-control sweeps only write).  The state is cut into tiles of
+// 2^12 amplitudes.  A tile's 12 "tile bits" are two contiguous physical ranges:
+// bits 0..C-1 (carried in every tile so each HBM access is a run of 2^C
+// amplitudes, C >= 3 -> >= 128 B) and bits q..q+11-C (the qubits mixed by this
+// sweep).  The low sweep has C = 12 (tile = 4096 consecutive amplitudes).
+//
+// A persistent CTA of 256 threads holds one tile in registers, 16 amplitudes
+// per thread, and re-maps it through shared memory between three register
+// groups of four tile bits:
+//   M2: registers = tile bits 8..11, threads = tile bits 0..7        (HBM load/store)
 //   M0: registers = tile bits 0..3,  threads = tile bits 4..11
-//   M1: registers = tile bits 4..7,  threads = tile bits 0..3, 8..11 (coalesced store)
-// RX butterflies on the register bits are register-local.  Between the RX
-// stages of one sweep it can apply the diagonal cost phase (table lookup by
-// the integer cut count C(x), recomputed from the row masks -- no table read
-// from HBM), a final scale and the <C> reduction.
+//   M1: registers = tile bits 4..7,  threads = tile bits 0..3, 8..11 (HBM store)
+// RX butterflies on register bits are register-local; tile bit 3 is lane bit 3
+// in both M2 and M1, so a lone active bit there is done with warp shuffles
+// instead of an extra shared-memory pass.  The diagonal cost phase (lookup of
+// exp(-i gamma (E - 2C)/2) by the integer cut count C(x), recomputed from the
+// row masks -- the cut table is never read from HBM), the fast-mode scale and
+// the <C> reduction are applied on the registers between / after the stages.
 //
 // Reference path replaced (pkg/src/qaoa_maxcut/):
 //   cost layer  apply_cost_bitwise  cost.py:162-176 (+ cut_counts :88-99)
@@ -28,290 +34,408 @@ constexpr int kTileBits = 12;
 constexpr int kTile = 1 << kTileBits;
 constexpr int kThreads = 256;
 constexpr int kRegs = 16;
-
-// Shared-memory slot of tile index t: one 16-byte pad after every 16 slots.
-// Every mapping's register r then sits at a compile-time offset from a
-// per-thread base (M2: +272 r, M0: +r, M1: +17 r) and each 8-lane phase of a
-// 128-bit access touches 8 distinct 16-byte bank groups (no conflicts).
+// Shared-memory slot of tile index t: one 16-byte pad after every 16 slots, so
+// register r of every mapping sits at a compile-time offset from a per-thread
+// base (M2: +272 r, M0: +r, M1: +17 r) and every 8-lane phase of a 128-bit
+// access hits 8 distinct 16-byte bank groups.
 constexpr int kSlots = kTile + kTile / 16;
-__device__ __forceinline__ int swz(int t) { return t + (t >> 4); }
+__host__ __device__ constexpr int slot(int t) { return t + (t >> 4); }
 
 // Tile index of register r of thread tid in mapping M.
 template <int M>
-__device__ __forceinline__ int tile_index(int tid, int r) {
-  if (M == 2) return tid | (r << 8);
-  if (M == 0) return (tid << 4) | r;
-  return (tid & 15) | ((tid >> 4) << 8) | (r << 4);
+__host__ __device__ constexpr int tile_index(int tid, int r) {
+  return M == 2 ? (tid | (r << 8))
+                : (M == 0 ? ((tid << 4) | r) : ((tid & 15) | ((tid >> 4) << 8) | (r << 4)));
 }
-
-__device__ __forceinline__ uint64_t tile_offset(int t, const int* pos) {
-  uint64_t o = 0;
-#pragma unroll
-  for (int k = 0; k < kTileBits; ++k)
-    if ((t >> k) & 1) o |= 1ull << pos[k];
-  return o;
-}
-
-// Global offsets of the 16 registers of mapping M relative to the thread's base:
-// subsets of the four strides of the register tile bits (4M+? see tile_index).
 template <int M>
-__device__ __forceinline__ void reg_strides(const int* pos, uint64_t (&s)[4]) {
-  constexpr int g = (M == 2) ? 8 : (M == 0 ? 0 : 4);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) s[k] = 1ull << pos[g + k];
+__host__ __device__ constexpr int slot_stride() {
+  return M == 2 ? 272 : (M == 0 ? 1 : 17);
+}
+template <int M>
+__host__ __device__ constexpr int group_of() {
+  return M == 2 ? 2 : (M == 0 ? 0 : 1);
 }
 
-__device__ __forceinline__ uint64_t reg_off(int r, const uint64_t (&s)[4]) {
-  uint64_t o = 0;
-  if (r & 1) o |= s[0];
-  if (r & 2) o |= s[1];
-  if (r & 4) o |= s[2];
-  if (r & 8) o |= s[3];
-  return o;
+// Physical offset of tile index t for carried-bit count C and high range at q.
+template <int C>
+__device__ __forceinline__ uint64_t tile_off(int t, uint64_t Q /* = 1 << q */) {
+  if (C >= 12) return (uint64_t)t;
+  return (uint64_t)(t & ((1 << C) - 1)) + (uint64_t)(t >> C) * Q;
+}
+template <int C>
+__device__ __forceinline__ int tile_pos(int k, int q) {  // physical bit of tile bit k
+  return (C >= 12 || k < C) ? k : q + (k - C);
 }
 
 template <int M>
-__device__ __forceinline__ void smem_store(double2* buf, const double2 (&v)[kRegs]) {
-  const int tid = threadIdx.x;
+__device__ __forceinline__ void smem_store(double2* buf, int sb, const double2 (&v)[kRegs]) {
 #pragma unroll
-  for (int r = 0; r < kRegs; ++r) buf[swz(tile_index<M>(tid, r))] = v[r];
+  for (int r = 0; r < kRegs; ++r) buf[sb + r * slot_stride<M>()] = v[r];
 }
-
 template <int M>
-__device__ __forceinline__ void smem_load(const double2* buf, double2 (&v)[kRegs]) {
-  const int tid = threadIdx.x;
+__device__ __forceinline__ void smem_load(const double2* buf, int sb, double2 (&v)[kRegs]) {
 #pragma unroll
-  for (int r = 0; r < kRegs; ++r) v[r] = buf[swz(tile_index<M>(tid, r))];
+  for (int r = 0; r < kRegs; ++r) v[r] = buf[sb + r * slot_stride<M>()];
 }
 
-// Re-map registers from mapping `from` to `to` through shared memory.  Each
-// thread later writes (in mapping `to`) exactly the slots it read here, so one
-// barrier per exchange suffices within a tile.
-__device__ __forceinline__ void exchange(double2* buf, double2 (&v)[kRegs], int from, int to) {
-  if (from == to) return;
-  if (from == 0) smem_store<0>(buf, v);
-  else if (from == 1) smem_store<1>(buf, v);
-  else smem_store<2>(buf, v);
+struct ThreadSlots {
+  int s0, s1, s2;
+};
+
+// Re-map registers from mapping A to mapping B through shared memory.  In a
+// later exchange every thread writes (in mapping B) exactly the slots it read
+// here, so one barrier per exchange suffices; the tile loop adds one barrier
+// before the first write of the next tile.
+template <int A, int B>
+__device__ __forceinline__ void exchange(double2* buf, const ThreadSlots& ts, double2 (&v)[kRegs]) {
+  smem_store<A>(buf, A == 0 ? ts.s0 : (A == 1 ? ts.s1 : ts.s2), v);
   __syncthreads();
-  if (to == 0) smem_load<0>(buf, v);
-  else if (to == 1) smem_load<1>(buf, v);
-  else smem_load<2>(buf, v);
+  smem_load<B>(buf, B == 0 ? ts.s0 : (B == 1 ? ts.s1 : ts.s2), v);
 }
 
-// RX on register bit K of all 16 registers.
-template <int K, int MODE>
-__device__ __forceinline__ void rx_bit(double2 (&v)[kRegs], double a, double b) {
-#pragma unroll
-  for (int r = 0; r < kRegs; ++r) {
-    if (r & (1 << K)) continue;
-    if (MODE == 0) rx_exact(v[r], v[r | (1 << K)], a, b);
-    else if (MODE == 1) rx_form1(v[r], v[r | (1 << K)], a);
-    else rx_form2(v[r], v[r | (1 << K)], a);
+// Compile-time description of which tile bits a sweep mixes: bits C..11 (C<12)
+// or all 12 (C == 12).
+template <int C>
+struct Act {
+  static constexpr unsigned tile = C >= 12 ? 0xFFFu : ((0xFFFu >> C) << C);
+  static constexpr unsigned g0 = tile & 15u;
+  static constexpr unsigned g1 = (tile >> 4) & 15u;
+  static constexpr unsigned g2 = (tile >> 8) & 15u;
+  // a lone active bit 3 in group 0 is handled by lane shuffles (lane bit 3 in M2 and M1)
+  static constexpr bool g0_shfl = (g0 == 8u);
+  static constexpr bool g0_xchg = g0 != 0 && !g0_shfl;
+};
+
+struct TileCtx {
+  uint64_t base;           // physical index of tile element 0 (tile bits zero), without x_hi
+  uint64_t tb0, tb1, tb2;  // thread base offsets per mapping
+};
+
+// Per-tile cut-count basis, computed once per CTA by warp 0 (lane-parallel over
+// nodes): K = C(h) for the tile's non-tile bits h (tile bits zero) and, per tile
+// node k, d[k] = deg(k) - 2 popc(adj[k] & h) = change of C when node k alone
+// flips.  adjl[k] = tile-local neighbour mask of tile node k (12 bits).
+struct CutBasis {
+  int K;
+  int d[12];
+  int adjl[12];
+};
+
+template <bool WIDE, int C>
+__device__ __forceinline__ void cut_basis(const SweepArgs& a, uint64_t h, int q, CutBasis* cb) {
+  const int lane = threadIdx.x & 31;
+  int part = 0;
+  for (int i = lane; i < a.g.n_nodes; i += 32) {
+    const uint64_t b = 0ull - ((h >> i) & 1ull);
+    part += __popcll(a.g.rm[i] & (b ^ h));
   }
-}
-
-template <int MODE>
-__device__ __forceinline__ void rx_group_mode(double2 (&v)[kRegs], unsigned act4, double a,
-                                              double b) {
-  if (act4 & 1) rx_bit<0, MODE>(v, a, b);
-  if (act4 & 2) rx_bit<1, MODE>(v, a, b);
-  if (act4 & 4) rx_bit<2, MODE>(v, a, b);
-  if (act4 & 8) rx_bit<3, MODE>(v, a, b);
-}
-
-// RX on the active bits of register group g (tile bits 4g..4g+3), in increasing order.
-__device__ __forceinline__ void rx_group(double2 (&v)[kRegs], unsigned act, int g,
-                                         const RxStage& st) {
-  const unsigned a4 = (act >> (4 * g)) & 15u;
-  if (!a4) return;
-  if (st.mode == 0) rx_group_mode<0>(v, a4, st.a, st.b);
-  else if (st.mode == 1) rx_group_mode<1>(v, a4, st.a, st.b);
-  else rx_group_mode<2>(v, a4, st.a, st.b);
-}
-
-// Base offset of the thread in mapping M (register bits zero).
-__device__ __forceinline__ uint64_t thread_base(int m, const int* pos) {
-  const int tid = threadIdx.x;
-  int t;
-  if (m == 2) t = tile_index<2>(tid, 0);
-  else if (m == 0) t = tile_index<0>(tid, 0);
-  else t = tile_index<1>(tid, 0);
-  return tile_offset(t, pos);
-}
-
-__device__ __forceinline__ void reg_positions(int m, const int* pos, int (&v)[4]) {
-  const int g = (m == 2) ? 8 : (m == 0 ? 0 : 4);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) v[k] = pos[g + k];
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane < 12) {
+    const int p = tile_pos<C>(lane, q);
+    const uint64_t m = a.g.adj[p];
+    cb->d[lane] = __popcll(m) - 2 * __popcll(m & h);
+    const uint32_t lo = (uint32_t)(m & ((C >= 12) ? 0xFFFull : ((1ull << C) - 1ull)));
+    const uint32_t hi = (C >= 12) ? 0u : (uint32_t)((m >> q) & ((1ull << (12 - C)) - 1ull)) << C;
+    cb->adjl[lane] = (int)(lo | hi);
+  }
+  if (lane == 0) cb->K = part;
 }
 
-template <bool WIDE>
-__device__ __forceinline__ void apply_cost_regs(double2 (&v)[kRegs], uint64_t x0, const int* pos,
-                                                int m, const GraphDev& g, const double2* tab) {
-  int vp[4];
-  reg_positions(m, pos, vp);
-  int c[16];
-  cut_counts16<WIDE>(x0, vp, g, c);
-  const int two_e = 2 * g.tot_edge;
+// C(x) for the 16 registers of mapping M: C(h | t) = K + sum_{k in t} d[k] - 2 E(t),
+// E(t) = edges among the set tile nodes of t.  Exact integer arithmetic.
+template <int M>
+__device__ __forceinline__ void cut16(const CutBasis* cb, int (&c)[16]) {
+  const int t = tile_index<M>(threadIdx.x, 0);
+  constexpr int g = group_of<M>();
+  int c0 = cb->K;
 #pragma unroll
-  for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], tab[two_e - 2 * c[r]]);
+  for (int k = 0; k < 12; ++k) {
+    if (k >= 4 * g && k < 4 * g + 4) continue;  // register bits are zero in t
+    if ((t >> k) & 1) c0 += cb->d[k] - __popc(cb->adjl[k] & t);
+  }
+  int d[4], al[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    al[j] = cb->adjl[4 * g + j];
+    d[j] = cb->d[4 * g + j] - 2 * __popc(al[j] & t);
+  }
+  const int a01 = 2 * ((al[0] >> (4 * g + 1)) & 1), a02 = 2 * ((al[0] >> (4 * g + 2)) & 1);
+  const int a03 = 2 * ((al[0] >> (4 * g + 3)) & 1), a12 = 2 * ((al[1] >> (4 * g + 2)) & 1);
+  const int a13 = 2 * ((al[1] >> (4 * g + 3)) & 1), a23 = 2 * ((al[2] >> (4 * g + 3)) & 1);
+  c[0] = c0;
+  c[1] = c0 + d[0];
+  c[2] = c0 + d[1];
+  c[3] = c[1] + d[1] - a01;
+  c[4] = c0 + d[2];
+  c[5] = c[1] + d[2] - a02;
+  c[6] = c[2] + d[2] - a12;
+  c[7] = c[3] + d[2] - a02 - a12;
+  c[8] = c0 + d[3];
+  c[9] = c[1] + d[3] - a03;
+  c[10] = c[2] + d[3] - a13;
+  c[11] = c[3] + d[3] - a03 - a13;
+  c[12] = c[4] + d[3] - a23;
+  c[13] = c[5] + d[3] - a03 - a23;
+  c[14] = c[6] + d[3] - a13 - a23;
+  c[15] = c[7] + d[3] - a03 - a13 - a23;
 }
 
-template <bool WIDE>
-__device__ __forceinline__ double expect_regs(const double2 (&v)[kRegs], uint64_t x0,
-                                              const int* pos, int m, const GraphDev& g) {
-  int vp[4];
-  reg_positions(m, pos, vp);
+// amp *= table_even[E - C(x)] (table_even[k] = phase_table[2k]; reference
+// cost.py:168-172 indexes table[(E - 2C) + E]).
+template <int M>
+__device__ __forceinline__ void apply_cost(double2 (&v)[kRegs], const CutBasis* cb,
+                                           const double2* __restrict__ tab, int e) {
   int c[16];
-  cut_counts16<WIDE>(x0, vp, g, c);
+  cut16<M>(cb, c);
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], __ldg(tab + (e - c[r])));
+}
+
+template <int M>
+__device__ __forceinline__ double expect_acc(const double2 (&v)[kRegs], const CutBasis* cb) {
+  int c[16];
+  cut16<M>(cb, c);
   double acc = 0.0;
 #pragma unroll
   for (int r = 0; r < kRegs; ++r) acc += (v[r].x * v[r].x + v[r].y * v[r].y) * (double)c[r];
   return acc;
 }
 
-template <bool WIDE>
-__global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const SweepArgs args) {
+// RX(stage) on register bits MASK: exact (reference rounding) or the factored
+// fast form mine - i t other (form-2 levels run as form 1 with t = -k plus a
+// global bit complement tracked on the host; see qaoa_capi.cu).
+template <unsigned MASK, bool EXACT>
+__device__ __forceinline__ void rx_regs2(double2 (&v)[kRegs], double c_or_t, double s) {
+#pragma unroll
+  for (int K = 0; K < 4; ++K) {
+    if (!((MASK >> K) & 1)) continue;
+#pragma unroll
+    for (int r = 0; r < kRegs; ++r) {
+      if (r & (1 << K)) continue;
+      if (EXACT) rx_exact(v[r], v[r | (1 << K)], c_or_t, s);
+      else rx_form1(v[r], v[r | (1 << K)], c_or_t);
+    }
+  }
+}
+
+template <bool EXACT>
+__device__ __forceinline__ void rx_lane3(double2 (&v)[kRegs], double c_or_t, double s) {
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    double2 o;
+    o.x = __shfl_xor_sync(0xffffffffu, v[r].x, 8);
+    o.y = __shfl_xor_sync(0xffffffffu, v[r].y, 8);
+    if (EXACT) {
+      const double nr = __dadd_rn(__dmul_rn(c_or_t, v[r].x), __dmul_rn(s, o.y));
+      const double ni = __dadd_rn(__dmul_rn(c_or_t, v[r].y), __dmul_rn(-s, o.x));
+      v[r].x = nr; v[r].y = ni;
+    } else {
+      const double nr = __fma_rn(c_or_t, o.y, v[r].x);
+      const double ni = __fma_rn(-c_or_t, o.x, v[r].y);
+      v[r].x = nr; v[r].y = ni;
+    }
+  }
+}
+
+template <int C, int M>
+__device__ __forceinline__ void store_tile(double2* __restrict__ amps, const TileCtx& tc,
+                                           uint64_t Q, const double2 (&v)[kRegs]) {
+  const uint64_t tb = M == 2 ? tc.tb2 : tc.tb1;
+  double2* dst = amps + tc.base + tb;
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) __stcs(dst + tile_off<C>(tile_index<M>(0, r), Q), v[r]);
+}
+
+// FLOW 0: exact (reference order: tile bits ascending, reference rounding)
+// FLOW 1: fast, one RX stage
+// FLOW 2: fast, RX stage -> cost -> RX stage (two levels in one sweep)
+// One 4096-amplitude tile per CTA; two CTAs per SM keep one tile's loads in
+// flight while the other computes (a persistent grid measured slower).
+template <bool WIDE, int C, int FLOW>
+__global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* buf = reinterpret_cast<double2*>(smem_raw);
-  double2* tab = buf + kSlots;
+  double2* buf = reinterpret_cast<double2*>(smem_raw);  // kSlots exchange slots
+  __shared__ CutBasis cb;
   __shared__ double red_scratch[kThreads / 32];
+  using A = Act<C>;
+  constexpr bool EX = FLOW == 0;
 
-  const uint32_t flags = args.flags;
-  const bool has_cost = flags & (kPreCost | kMidCost);
-  double2* tab2 = tab + ((flags & kPreCost) ? args.table_len : 0);
-  if (flags & kPreCost)
-    for (int i = threadIdx.x; i < args.table_len; i += kThreads) tab[i] = args.table[i];
-  if (flags & kMidCost)
-    for (int i = threadIdx.x; i < args.table_len; i += kThreads) tab2[i] = args.table2[i];
-  // tile_offsets of each mapping's thread base (constant over tiles)
-  const uint64_t tb0 = thread_base(0, args.pos);
-  const uint64_t tb1 = thread_base(1, args.pos);
-  const uint64_t tb2 = thread_base(2, args.pos);
-  uint64_t s2[4], s1[4];
-  reg_strides<2>(args.pos, s2);
-  reg_strides<1>(args.pos, s1);
-  const bool exact = flags & kExact;
-  double acc = 0.0;
-  double2* __restrict__ amps = args.amps;
-
+  const uint32_t flags = a.flags;
+  const int tid = threadIdx.x;
+  const int q = a.q;
+  const uint64_t Q = 1ull << (C >= 12 ? 0 : q);
+  const uint64_t tile = blockIdx.x;
+  TileCtx tc;
   {
-    const int64_t tile = blockIdx.x;
-    // base: deposit the tile number into the non-tile bit positions
-    uint64_t base = (uint64_t)tile;
-#pragma unroll
-    for (int k = 0; k < kTileBits; ++k) {
-      const int p = args.ins[k];
-      base = ((base >> p) << (p + 1)) | (base & ((1ull << p) - 1ull));
-    }
-    if (has_cost) __syncthreads();  // phase table staged
+    const int low_bits = C >= 12 ? 0 : q - C;  // non-tile ranges [C, q) and [q + 12 - C, n)
+    tc.base = C >= 12 ? (tile << 12)
+                      : (((tile & ((1ull << low_bits) - 1ull)) << C) | ((tile >> low_bits) << (q + 12 - C)));
+  }
+  tc.tb2 = tile_off<C>(tile_index<2>(tid, 0), Q);
+  tc.tb1 = tile_off<C>(tile_index<1>(tid, 0), Q);
+  ThreadSlots ts;
+  ts.s2 = slot(tile_index<2>(tid, 0));
+  ts.s1 = slot(tile_index<1>(tid, 0));
+  ts.s0 = slot(tile_index<0>(tid, 0));
+  double2* __restrict__ amps = a.amps;
 
-    double2 v[kRegs];
-    int cur = 2;
-    if (flags & kGen) {
+  double2 v[kRegs];
+  if (flags & kGen) {
 #pragma unroll
-      for (int r = 0; r < kRegs; ++r) v[r] = args.gen;
-    } else {
-      const double2* src = amps + base + tb2;
+    for (int r = 0; r < kRegs; ++r) v[r] = a.gen;
+  } else {
+    const double2* src = amps + tc.base + tc.tb2;
 #pragma unroll
-      for (int r = 0; r < kRegs; ++r) v[r] = __ldcs(src + reg_off(r, s2));
-    }
-    if (flags & kPreCost)
-      apply_cost_regs<WIDE>(v, args.g.x_hi | base | tb2, args.pos, 2, args.g, tab);
+    for (int r = 0; r < kRegs; ++r) v[r] = __ldcs(src + tile_off<C>(tile_index<2>(0, r), Q));
+  }
+  const bool need_cut = flags & (kPreCost | kMidCost | kExpect);
+  if (need_cut) {
+    if (tid < 32) cut_basis<WIDE, C>(a, a.g.x_hi | tc.base, q, &cb);
+    __syncthreads();
+  }
+  const int e = a.g.tot_edge;
+  const double r1a = a.rx1.a, r1b = a.rx1.b, r2a = a.rx2.a;
+  double acc = 0.0;
 
-    if (exact) {
-      if (flags & kStage1) {
-        for (int grp = 0; grp < 3; ++grp) {
-          if (!((args.act1 >> (4 * grp)) & 15u)) continue;
-          exchange(buf, v, cur, grp);
-          cur = grp;
-          rx_group(v, args.act1, grp, args.rx1);
-        }
-      }
+  if (FLOW == 0) {
+    // ---- exact: cost first (level start), then tile bits in increasing order
+    if (flags & kPreCost) apply_cost<2>(v, &cb, a.table, e);
+    if (C >= 12) {
+      exchange<2, 0>(buf, ts, v);
+      rx_regs2<A::g0, true>(v, r1a, r1b);
+      exchange<0, 1>(buf, ts, v);
+      rx_regs2<A::g1, true>(v, r1a, r1b);
+      exchange<1, 2>(buf, ts, v);
     } else {
-      if (flags & kStage1) {
-        const int order[3] = {2, 0, 1};
+      if (A::g0_shfl) rx_lane3<true>(v, r1a, r1b);
+      if (A::g1) {
+        exchange<2, 1>(buf, ts, v);
+        rx_regs2<A::g1, true>(v, r1a, r1b);
+        exchange<1, 2>(buf, ts, v);
+      }
+    }
+    rx_regs2<A::g2, true>(v, r1a, r1b);
+    if (flags & kExpect) acc = expect_acc<2>(v, &cb);
+    store_tile<C, 2>(amps, tc, Q, v);
+  } else if (C >= 12) {
+    // ---- fast, low set: G2 (loaded), G0, G1 [, cost, G1, G0, G2]
+    if (flags & kPreCost) apply_cost<2>(v, &cb, a.table, e);
+    rx_regs2<A::g2, false>(v, r1a, 0.0);
+    exchange<2, 0>(buf, ts, v);
+    rx_regs2<A::g0, false>(v, r1a, 0.0);
+    exchange<0, 1>(buf, ts, v);
+    rx_regs2<A::g1, false>(v, r1a, 0.0);
+    if (FLOW == 2) {
+      apply_cost<1>(v, &cb, a.table2, e);
+      rx_regs2<A::g1, false>(v, r2a, 0.0);
+      exchange<1, 0>(buf, ts, v);
+      rx_regs2<A::g0, false>(v, r2a, 0.0);
+      exchange<0, 2>(buf, ts, v);
+      rx_regs2<A::g2, false>(v, r2a, 0.0);
+      if (flags & kScale) {
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          const int grp = order[i];
-          if (!((args.act1 >> (4 * grp)) & 15u)) continue;
-          exchange(buf, v, cur, grp);
-          cur = grp;
-          rx_group(v, args.act1, grp, args.rx1);
-        }
+        for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
       }
-      if (flags & kMidCost) {
-        const uint64_t tb = cur == 0 ? tb0 : (cur == 1 ? tb1 : tb2);
-        apply_cost_regs<WIDE>(v, args.g.x_hi | base | tb, args.pos, cur, args.g, tab2);
+      if (flags & kExpect) acc = expect_acc<2>(v, &cb);
+      store_tile<C, 2>(amps, tc, Q, v);
+    } else {
+      if (flags & kScale) {
+#pragma unroll
+        for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
       }
-      if (flags & kStage2) {
-        // current mapping first (no exchange), M0 in the middle, end on a
-        // mapping whose stores coalesce (M1 or M2)
-        int ord[3];
-        if (cur == 0) { ord[0] = 0; ord[1] = 1; ord[2] = 2; }
-        else { ord[0] = cur; ord[1] = 0; ord[2] = 3 - cur; }
-        for (int i = 0; i < 3; ++i) {
-          const int grp = ord[i];
-          if (!((args.act2 >> (4 * grp)) & 15u)) continue;
-          exchange(buf, v, cur, grp);
-          cur = grp;
-          rx_group(v, args.act2, grp, args.rx2);
-        }
-      }
+      if (flags & kExpect) acc = expect_acc<1>(v, &cb);
+      store_tile<C, 1>(amps, tc, Q, v);
     }
-    if (cur == 0) {  // M0 stores are not coalesced
-      exchange(buf, v, 0, 2);
-      cur = 2;
+  } else {
+    // ---- fast, high set: G2 (+ lane bit 3), G1 [, cost, G1 (+ lane bit 3), G2]
+    if (flags & kPreCost) apply_cost<2>(v, &cb, a.table, e);
+    rx_regs2<A::g2, false>(v, r1a, 0.0);
+    if (A::g0_shfl) rx_lane3<false>(v, r1a, 0.0);
+    if (A::g1) {
+      exchange<2, 1>(buf, ts, v);
+      rx_regs2<A::g1, false>(v, r1a, 0.0);
+      if (FLOW == 2) {
+        apply_cost<1>(v, &cb, a.table2, e);
+        rx_regs2<A::g1, false>(v, r2a, 0.0);
+        if (A::g0_shfl) rx_lane3<false>(v, r2a, 0.0);
+        exchange<1, 2>(buf, ts, v);
+        rx_regs2<A::g2, false>(v, r2a, 0.0);
+      }
+    } else if (FLOW == 2) {
+      apply_cost<2>(v, &cb, a.table2, e);
+      rx_regs2<A::g2, false>(v, r2a, 0.0);
+      if (A::g0_shfl) rx_lane3<false>(v, r2a, 0.0);
     }
+    constexpr int last = (A::g1 && FLOW == 1) ? 1 : 2;
     if (flags & kScale) {
 #pragma unroll
-      for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], args.scale);
+      for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
     }
-    const uint64_t tb = cur == 1 ? tb1 : tb2;
-    if (flags & kExpect) acc += expect_regs<WIDE>(v, args.g.x_hi | base | tb, args.pos, cur, args.g);
-    if (!(flags & kNoStore)) {
-      double2* dst = amps + base + tb;
-      if (cur == 1) {
-#pragma unroll
-        for (int r = 0; r < kRegs; ++r) __stcs(dst + reg_off(r, s1), v[r]);
-      } else {
-#pragma unroll
-        for (int r = 0; r < kRegs; ++r) __stcs(dst + reg_off(r, s2), v[r]);
-      }
-    }
+    if (flags & kExpect) acc = expect_acc<last>(v, &cb);
+    store_tile<C, last>(amps, tc, Q, v);
   }
   if (flags & kExpect) {
     const double t = block_sum<kThreads>(acc, red_scratch);
-    if (threadIdx.x == 0) args.partials[blockIdx.x] = t;
+    if (threadIdx.x == 0) a.partials[blockIdx.x] = t;
   }
 }
 
-size_t sweep_smem_bytes(int table_len) {
-  return (size_t)kSlots * sizeof(double2) + (size_t)table_len * sizeof(double2);
-}
+size_t sweep_smem_bytes(int) { return (size_t)kSlots * sizeof(double2); }
 
-cudaError_t launch_sweep(const SweepArgs& args, int grid, cudaStream_t stream) {
-  const int n_tables = ((args.flags & kPreCost) ? 1 : 0) + ((args.flags & kMidCost) ? 1 : 0);
-  const size_t smem = sweep_smem_bytes(n_tables * args.table_len);
-  if (args.g.n_nodes > 32) {
-    cudaFuncSetAttribute(sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sweep_kernel<true><<<grid, kThreads, smem, stream>>>(args);
-  } else {
-    cudaFuncSetAttribute(sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sweep_kernel<false><<<grid, kThreads, smem, stream>>>(args);
+template <bool WIDE, int C, int FLOW>
+static cudaError_t launch_one(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<WIDE, C, FLOW>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
   }
+  sweep_kernel<WIDE, C, FLOW><<<grid, kThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 
-int sweep_max_grid(int table_len) {
-  const size_t smem = sweep_smem_bytes(table_len);
+template <bool WIDE, int C>
+static cudaError_t launch_c(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {
+  if (a.flags & kExact) return launch_one<WIDE, C, 0>(a, grid, smem, s);
+  if (a.flags & kStage2) return launch_one<WIDE, C, 2>(a, grid, smem, s);
+  return launch_one<WIDE, C, 1>(a, grid, smem, s);
+}
+
+template <bool WIDE>
+static cudaError_t launch_w(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {
+  switch (a.carry) {
+    case 3: return launch_c<WIDE, 3>(a, grid, smem, s);
+    case 4: return launch_c<WIDE, 4>(a, grid, smem, s);
+    case 5: return launch_c<WIDE, 5>(a, grid, smem, s);
+    case 6: return launch_c<WIDE, 6>(a, grid, smem, s);
+    case 7: return launch_c<WIDE, 7>(a, grid, smem, s);
+    case 8: return launch_c<WIDE, 8>(a, grid, smem, s);
+    case 9: return launch_c<WIDE, 9>(a, grid, smem, s);
+    case 10: return launch_c<WIDE, 10>(a, grid, smem, s);
+    case 11: return launch_c<WIDE, 11>(a, grid, smem, s);
+    case 12: return launch_c<WIDE, 12>(a, grid, smem, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_sweep(const SweepArgs& a, int grid, cudaStream_t stream) {
+  const int n_tables = ((a.flags & kPreCost) ? 1 : 0) + ((a.flags & kStage2) ? 1 : 0);
+  const size_t smem = sweep_smem_bytes(n_tables * a.table_len);
+  return a.g.n_nodes > 32 ? launch_w<true>(a, grid, smem, stream)
+                          : launch_w<false>(a, grid, smem, stream);
+}
+
+int sweep_max_grid(int) {
   int dev = 0;
   cudaGetDevice(&dev);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int per_sm = 0;
-  cudaFuncSetAttribute(sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<false>, kThreads, smem);
+  const size_t smem = sweep_smem_bytes(0);
+  cudaFuncSetAttribute(sweep_kernel<false, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<false, 3, 2>, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
   return sms * per_sm;
 }

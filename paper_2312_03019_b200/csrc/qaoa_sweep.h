@@ -21,14 +21,13 @@ enum SweepFlags : uint32_t {
 
 struct SweepArgs {
   double2* amps;
-  const double2* table;  // phase table (2E+1) of the pre-stage cost step
-  const double2* table2; // phase table (2E+1) of the mid cost step
+  const double2* table;  // even phase-table entries (E+1) of the pre-stage cost step
+  const double2* table2; // even phase-table entries (E+1) of the mid cost step
   double* partials;      // [grid] block partial sums (kExpect)
   GraphDev g;
   int64_t ntiles;        // 2^(n_local - 12)
-  int pos[12];           // physical bit of tile bit k (pos[0..2] = 0,1,2)
-  int ins[12];           // the same positions sorted ascending (tile-number deposit)
-  unsigned act1, act2;   // active tile bits of the two RX stages
+  int carry;             // C: tile bits 0..C-1 = physical bits 0..C-1 (12 = low sweep)
+  int q;                 // tile bits C..11 = physical bits q..q+11-C (the mixed qubits)
   RxStage rx1, rx2;
   double2 gen;
   double2 scale;
@@ -50,8 +49,8 @@ cudaError_t launch_expectation(const double2* amps, int n_local, const GraphDev&
                                double* partials, int grid, cudaStream_t s);
 cudaError_t launch_norm_sq(const double2* amps, uint64_t n, double* partials, int grid,
                            cudaStream_t s);
-cudaError_t launch_max_abs_diff(const double2* a, const double2* b, uint64_t n, double* partials,
-                                int grid, cudaStream_t s);
+cudaError_t launch_max_abs_diff(const double2* a, const double2* b, uint64_t n, uint64_t xmask,
+                                double* partials, int grid, cudaStream_t s);
 cudaError_t launch_sum_partials(const double* partials, int n, double* out, int mode_max,
                                 cudaStream_t s);
 cudaError_t launch_cut_table(void* table, int bytes_per, int n_local, const GraphDev& g,
