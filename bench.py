@@ -1,0 +1,351 @@
+#!/usr/bin/env python3
+"""Benchmark: QAOA Max-Cut levels/s and amplitude-updates/s on B200.
+
+Workload (BASELINE.json configs[2], the roofline configuration; configs[1]
+N=26 p=4 is a parity-test case): random 3-regular graph N=30 (seed 0),
+p=10 levels with params_from_seed(10, 0) (reference bench.py:61-67), complex128
+state of 16 GiB, launch-control init, fused <C>.  One "step" = one full
+``simulate`` (p levels) + ``expectation`` with the graph and angles already on
+the device.  The 16 GiB state is far larger than L2 (126 MB), so no flush is
+needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--n 30] [--p 10] [--exact]
+
+N > 1 (one process per GPU via torch.distributed.run): every rank runs its own
+full N-qubit state (weak scaling, "replicas": the sharded multi-GPU engine is
+exercised by its own tests).  Device time is the max over ranks.
+
+``--impl reference`` times the CPU oracle (oracle/, a C restatement of the
+reference's algorithm, bit-exact with it) on all host threads: each step is one
+level of the same graph family at N=28 (a bounded sample; the rate is converted
+to N=30 levels/s by the (N+1) 2^N amplitude-update count).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QAOA layers/sec and amplitude-updates/sec at N qubits; % HBM roofline; 1/2/4/8 GPU"
+UNIT = "layers/s"
+REF_SAMPLE_N = 28
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def init_dist(world: int, local: int):
+    if world <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return dist
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def ncu_traffic(n: int):
+    """dram read+write bytes per sweep launch from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        rec = d.get(str(n))
+        return float(rec["dram_bytes_per_launch"]) if rec else None
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_reference_rate(threads: int, levels: int = 1):
+    """Oracle (C port of the reference, bit-exact with it) on the host: amplitude
+    updates per second over `levels` levels of u3r N=28 (init + cost + mixer)."""
+    from oracle import oracle as O
+
+    n = REF_SAMPLE_N
+    edges = O.random_regular_edges(n, 3, 0)
+    rm = O.row_masks(n, edges)
+    gm, bt = O.params_from_seed(10, 0)
+    t0 = time.perf_counter()
+    amps = O.simulate(n, rm, len(edges), gm[:levels], bt[:levels], threads=threads)
+    dt = time.perf_counter() - t0
+    del amps
+    return levels * (n + 1) * (1 << n) / dt, dt
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+
+    O.lib()
+    threads = len(os.sched_getaffinity(0))
+    n, p = args.n, args.p
+    per_level = (n + 1) * (1 << n)
+    for _ in range(args.warmup):
+        cpu_reference_rate(threads)
+    rates, secs = [], 0.0
+    for _ in range(args.steps):
+        r, dt = cpu_reference_rate(threads)
+        rates.append(r)
+        secs += dt
+    rate = statistics.median(rates)
+    layers = rate / per_level
+    line = {
+        "impl": "reference", "metric": METRIC, "value": layers, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * p / layers, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"u3r N={n} seed 0, p={p} levels, complex128 (BASELINE configs[2])",
+                   "n_qubits": n, "p": p, "graph": "random 3-regular seed 0",
+                   "l2": "state >> L2 (16 GiB)"},
+        "amp_updates_per_s": rate,
+        "cpu_baseline": {"value": layers, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"1 level (init+cost+mixer) of u3r N={REF_SAMPLE_N} per step, "
+                                   f"rate scaled to N={n} by (N+1)2^N amplitude updates"},
+        "e2e": {"value": layers, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, rank: int, world: int, local: int):
+    import torch
+
+    import paper_2312_03019_b200 as Q
+    from paper_2312_03019_b200 import _lib
+
+    dist = init_dist(world, local)
+    device = local if world > 1 else 0
+    torch.cuda.set_device(device)
+    n, p = args.n, args.p
+    g = Q.random_regular_graph(n, 3, seed=0)
+    params = Q.params_from_seed(p, 0)  # same RNG stream as reference bench.py:61-67
+    tables, cs, ss = Q.level_arrays(g, params)
+    stream = torch.cuda.Stream(device)
+    eng = Q.Engine(n, device, stream=stream.cuda_stream)
+    eng.ensure_graph(g)
+    flags = _lib.RUN_EXPECTATION | _lib.RUN_TIMING | (_lib.RUN_EXACT if args.exact else 0)
+    L = _lib.load()
+
+    def step():
+        eng.call("qaoa_run_layers", p, _lib.dptr(tables.view(np.float64)), _lib.dptr(cs),
+                 _lib.dptr(ss), flags)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    expect_val = eng.scalar("qaoa_expectation")
+
+    # ---- device-timed region: K steps, events on the engine's stream -------
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launch_ms: list[float] = []
+    launches = 0
+    with ClockSampler(device) as clocks:
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+            buf = (ctypes.c_float * 4096)()
+            k = L.qaoa_layer_timings(eng.ptr, buf, 4096)
+            launch_ms.extend(buf[:k])
+            nl, hb = ctypes.c_int(), ctypes.c_double()
+            L.qaoa_last_run_stats(eng.ptr, ctypes.byref(nl), ctypes.byref(hb))
+            launches += nl.value
+        stop.record(stream)
+        torch.cuda.synchronize(device)
+    if dist:
+        dist.barrier()
+    dev_ms = start.elapsed_time(stop)
+    if dist:
+        t = torch.tensor([dev_ms], device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+    layers_per_s = world * p * args.steps / (dev_ms * 1e-3)
+    per_level = (n + 1) * (1 << n)
+    sweep_bytes = hb.value  # algorithmic bytes of the last step's sweeps
+    sweeps_per_step = len(launch_ms) // max(args.steps, 1)
+
+    # ---- roofline of the sweep kernel (the only kernel on the step's path
+    # apart from one tiny partial-sum reduction) ------------------------------
+    peak, peak_kind = measured_peaks()
+    step_sweep_ms = sum(launch_ms) / max(args.steps, 1)
+    achieved = sweep_bytes / (step_sweep_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(n)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "peak_kind": peak_kind,
+                "kernel": "qb::sweep_kernel (fused cost+RX sweep)",
+                "algorithmic_bytes_per_launch": 32 * (1 << n),
+                "launches_per_step": sweeps_per_step,
+                "avg_launch_ms": step_sweep_ms / max(sweeps_per_step, 1),
+                "level_roofline_frac_R3": (32 * 3 * (1 << n) * p / (dev_ms / args.steps * 1e-3))
+                / 1e9 / peak}
+
+    # ---- end to end through the public API: host inputs -> <C> on the host ----
+    e2e = None
+    if args.e2e_steps > 0:
+        s = Q.StateVector(n, engine=eng)
+        torch.cuda.synchronize(device)
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            # host -> device: graph masks + phase tables + RX coefficients (pinned)
+            eng.graph_key = None
+            sv = Q.simulate(g, params, "bitwise", max_qubits=n, state=s, exact=args.exact)
+            val = Q.expectation(g, sv)  # device -> host: <C>
+        e2e_s = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([e2e_s], device=f"cuda:{device}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        h2d = 8 * n + tables.nbytes + cs.nbytes + ss.nbytes
+        e2e = {"value": world * p * args.e2e_steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8,
+               "api": "paper_2312_03019_b200.simulate + expectation"}
+        assert abs(val - expect_val) <= 1e-10 * abs(expect_val)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = len(os.sched_getaffinity(0))
+            rate, dt = cpu_reference_rate(threads)
+            cpu = {"value": rate / per_level, "unit": UNIT, "cores": threads, "kind": "port",
+                   "sample": f"1 level of u3r N={REF_SAMPLE_N} on the oracle (C port, "
+                             f"{threads} OpenMP threads, {dt:.1f} s), scaled to N={n} levels/s",
+                   "amp_updates_per_s": rate}
+        except Exception as exc:  # the CPU baseline must never sink the GPU line
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": layers_per_s, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": f"u3r N={n} seed 0, p={p} levels, complex128 (BASELINE configs[2])",
+                       "n_qubits": n, "p": p, "graph": "random 3-regular seed 0",
+                       "schedule": "exact" if args.exact else "fast",
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "no flush: 16 GiB state >> 126 MB L2"},
+            "amp_updates_per_s": layers_per_s * per_level,
+            "expectation": expect_val,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=30)
+    ap.add_argument("--p", type=int, default=10)
+    ap.add_argument("--exact", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -52,6 +52,16 @@ class QaoaParams:
         return len(self.gamma)
 
 
+def params_from_seed(p: int, seed: int) -> QaoaParams:
+    """Seeded angle schedule of the reference's benchmark harness (bench.py:61-67):
+    default_rng(seed), gamma ~ U[0, 2pi) drawn first, then beta ~ U[0, pi)."""
+    rng = np.random.default_rng(seed)
+    return QaoaParams(
+        gamma=tuple(float(v) for v in rng.uniform(0.0, 2.0 * math.pi, p)),
+        beta=tuple(float(v) for v in rng.uniform(0.0, math.pi, p)),
+    )
+
+
 def validate_backend(backend: str, g: Graph | None = None) -> str:
     """circuit.py:34-39."""
     if backend not in BACKENDS:

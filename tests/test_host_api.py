@@ -128,3 +128,11 @@ def test_level_arrays_shape():
     t, cs, ss = Q.level_arrays(g, pr)
     assert t.shape == (2, 2 * g.tot_edge + 1) and t.dtype == np.complex128
     assert cs[1] == math.cos(-0.3) and ss[0] == math.sin(-0.25)
+
+
+def test_params_from_seed_matches_reference(golden):
+    meta, _ = golden
+    for key, pr in meta["params"].items():
+        p = int(key[1:].split("_")[0])
+        q = Q.params_from_seed(p, 0)
+        assert list(q.gamma) == pr["gamma"] and list(q.beta) == pr["beta"]
