@@ -105,6 +105,20 @@ QAOA_API int qaoa_apply_rx(qaoa_ctx* ctx, int qubit, double c, double s);
  * increasing order, c = cos(-beta/2), s = sin(-beta/2).  Bit-exact. */
 QAOA_API int qaoa_apply_mixer(qaoa_ctx* ctx, double c, double s);
 
+/* RX on the contiguous qubit range [q0, q0+count) in ONE fused sweep (count <= 9,
+ * q0 >= 12 - count, n >= 12; otherwise per-qubit kernels).  Used by the sharded
+ * driver for the qubits that arrive from the shard exchange.  flags:
+ * QAOA_RUN_EXACT for reference arithmetic, else the factored fast form (which
+ * may toggle the range's bits in the complement mask, see qaoa_get_cmask). */
+QAOA_API int qaoa_apply_rx_range(qaoa_ctx* ctx, int q0, int count, double c, double s, int flags);
+
+/* Complement mask of the stored state: the amplitude of true basis index x is
+ * stored at physical index x ^ cmask (fast-mode bookkeeping; bits >= n_local are
+ * shard bits maintained by a sharded host).  read/write_amplitudes map the local
+ * bits themselves. */
+QAOA_API int qaoa_get_cmask(qaoa_ctx* ctx, uint64_t* out);
+QAOA_API int qaoa_set_cmask(qaoa_ctx* ctx, uint64_t cmask);
+
 /* The fused p-level circuit (simulate(..., "bitwise"), circuit.py:97-113):
  * |+>^n (unless QAOA_RUN_FROM_STATE), then per level l: cost with
  * phase_tables[l] (2E+1 complex), mixer with (c[l], s[l]).

@@ -53,6 +53,11 @@ def lib():
         L.orc_norm.argtypes = [ctypes.c_int, _f64p, ctypes.c_int]
         L.orc_norm.restype = ctypes.c_double
         L.orc_max_threads.restype = ctypes.c_int
+        L.orc_apply_cost_x.argtypes = [ctypes.c_int, ctypes.c_int, _u64p, ctypes.c_uint64,
+                                       ctypes.c_int, _f64p, _f64p, ctypes.c_int]
+        L.orc_expectation_x.argtypes = [ctypes.c_int, ctypes.c_int, _u64p, ctypes.c_uint64, _f64p,
+                                        ctypes.c_int]
+        L.orc_expectation_x.restype = ctypes.c_double
         _lib = L
     return _lib
 
@@ -143,6 +148,61 @@ def expectation(n: int, row_mask, amps: np.ndarray, threads: int = 0) -> float:
 def norm(n: int, amps: np.ndarray, threads: int = 0) -> float:
     """state.py:50-51."""
     return float(lib().orc_norm(n, _ptr(amps, _f64p), threads))
+
+
+class OracleShard:
+    """CPU shard for the sharded-host tests (paper_2312_03019_b200.sharded.Shard
+    protocol): reference arithmetic on a numpy shard of global indices x_hi | y."""
+
+    def __init__(self, n_local: int, rank: int, threads: int = 1):
+        import torch
+
+        self.rank = rank
+        self.n = n_local
+        self.threads = threads
+        self.t = torch.zeros(1 << n_local, dtype=torch.complex128)
+        self.masks = None
+        self.n_nodes = 0
+        self.tot_edge = 0
+        self.x_hi = 0
+
+    def set_graph(self, n_nodes, masks, tot_edge, x_hi):
+        self.n_nodes, self.tot_edge, self.x_hi = n_nodes, tot_edge, x_hi
+        self.masks = _masks(masks)
+
+    def _amps(self):
+        return self.t.numpy()
+
+    def run_level(self, table, c, s, first):
+        a = self._amps()
+        if first:
+            a[:] = math.sqrt(1.0 / (1 << self.n_nodes))
+        tab = np.ascontiguousarray(table, dtype=np.complex128)
+        lib().orc_apply_cost_x(self.n, self.n_nodes, _ptr(self.masks, _u64p), self.x_hi,
+                               self.tot_edge, _ptr(tab, _f64p), _ptr(a, _f64p), self.threads)
+        lib().orc_apply_mixer(self.n, c, s, _ptr(a, _f64p), self.threads)
+
+    def apply_rx_range(self, q0, count, c, s):
+        a = self._amps()
+        for q in range(q0, q0 + count):
+            lib().orc_apply_rx(self.n, q, c, s, _ptr(a, _f64p), self.threads)
+
+    def get_cmask(self):
+        return 0
+
+    def set_cmask(self, m):
+        assert m == 0
+
+    def expectation(self):
+        a = self._amps()
+        return float(lib().orc_expectation_x(self.n, self.n_nodes, _ptr(self.masks, _u64p),
+                                             self.x_hi, _ptr(a, _f64p), self.threads))
+
+    def tensor(self):
+        return self.t
+
+    def synchronize(self):
+        pass
 
 
 # ---------------------------------------------------------------------------

@@ -158,6 +158,38 @@ ORC_EXPORT double orc_expectation(int n, const uint64_t* row_mask, const double*
     return total;
 }
 
+/* Shard variants for the sharded-host tests: the local state holds global
+ * basis indices x_hi | y (y < 2^n_local) of an n_nodes-node graph.  Same
+ * arithmetic as orc_apply_cost / orc_expectation (cost.py:162-176,
+ * circuit.py:116-121). */
+ORC_EXPORT void orc_apply_cost_x(int n_local, int n_nodes, const uint64_t* row_mask, uint64_t x_hi,
+                                 int tot_edge, const double* table, double* amps, int threads) {
+    const int64_t size = (int64_t)1 << n_local;
+    threads = set_threads(threads);
+#pragma omp parallel for schedule(static) num_threads(threads)
+    for (int64_t y = 0; y < size; ++y) {
+        const int64_t c = cut_count_one(n_nodes, row_mask, x_hi | (uint64_t)y);
+        const int64_t k = (int64_t)tot_edge - 2 * c + tot_edge;
+        const double pr = table[2 * k], pi = table[2 * k + 1];
+        const double ar = amps[2 * y], ai = amps[2 * y + 1];
+        amps[2 * y] = fma(ar, pr, -(ai * pi));
+        amps[2 * y + 1] = fma(ar, pi, ai * pr);
+    }
+}
+
+ORC_EXPORT double orc_expectation_x(int n_local, int n_nodes, const uint64_t* row_mask,
+                                    uint64_t x_hi, const double* amps, int threads) {
+    const int64_t size = (int64_t)1 << n_local;
+    double total = 0.0;
+    threads = set_threads(threads);
+#pragma omp parallel for schedule(static) reduction(+ : total) num_threads(threads)
+    for (int64_t y = 0; y < size; ++y) {
+        const double ar = amps[2 * y], ai = amps[2 * y + 1];
+        total += (ar * ar + ai * ai) * (double)cut_count_one(n_nodes, row_mask, x_hi | (uint64_t)y);
+    }
+    return total;
+}
+
 /* StateVector.norm, state.py:50-51. */
 ORC_EXPORT double orc_norm(int n, const double* amps, int threads) {
     const int64_t size = (int64_t)1 << n;

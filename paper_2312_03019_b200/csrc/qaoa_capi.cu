@@ -85,10 +85,10 @@ struct qaoa_ctx {
   size_t d_tables_cap = 0;  // in double2
   double2* h_tables = nullptr;  // pinned staging
   size_t h_tables_cap = 0;
-  // fast runs apply form-2 levels as form 1 + a global bit complement (X on
-  // every qubit commutes with the cost diagonal, C(~x) = C(x), and with RX):
-  // when set, the true amplitude of index x is stored at ~x.
-  bool complemented = false;
+  // fast runs apply form-2 RX levels as form 1 plus an X on every mixed qubit,
+  // done by bookkeeping: the true amplitude of index x is stored at x ^ cmask
+  // (g.cmask; X commutes with every RX, and the cost kernels evaluate C at the
+  // true index).  Bits >= n are the shard bits (managed by the sharded host).
   // expectation cached from the last fused run
   bool expect_valid = false;
   double expect_value = 0.0;
@@ -100,6 +100,8 @@ struct qaoa_ctx {
 };
 
 namespace {
+
+uint64_t local_mask(const qaoa_ctx* c) { return c->n >= 64 ? ~0ull : ((1ull << c->n) - 1ull); }
 
 int check_ctx(qaoa_ctx* c) {
   if (!c) return fail(QAOA_E_INVALID, "null context");
@@ -357,7 +359,9 @@ int qaoa_set_graph(qaoa_ctx* c, int n_nodes, const uint64_t* row_mask, int tot_e
     edges += __builtin_popcountll(m);
   }
   if (edges != tot_edge) return fail(QAOA_E_INVALID, "tot_edge does not match the row masks");
+  const uint64_t cmask = c->g.cmask;
   fill_graph(c->g, n_nodes, row_mask, tot_edge, x_hi);
+  c->g.cmask = cmask;
   c->has_graph = true;
   c->expect_valid = false;
   if (c->cut_table) {
@@ -375,8 +379,16 @@ int qaoa_init_uniform(qaoa_ctx* c) {
   CUDA_TRY(launch_fill(c->amps, 1ull << c->n, make_double2(u, 0.0), c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   c->expect_valid = false;
-  c->complemented = false;
+  c->g.cmask = 0;
   return QAOA_OK;
+}
+
+// Host-side index mapping for a stored state with local complement mask m:
+// true index x lives at x ^ m.  m = 0 or all-ones (single GPU) are a plain copy
+// or a reversal; other masks (sharded intermediate states) gather on the host.
+static void permute_chunk(double2* dst, const double2* src, uint64_t true_off, uint64_t count,
+                          uint64_t m, uint64_t stored_off) {
+  for (uint64_t i = 0; i < count; ++i) dst[i] = src[((true_off + i) ^ m) - stored_off];
 }
 
 int qaoa_write_amplitudes(qaoa_ctx* c, uint64_t offset, uint64_t count, const double* src) {
@@ -386,15 +398,26 @@ int qaoa_write_amplitudes(qaoa_ctx* c, uint64_t offset, uint64_t count, const do
   if (offset + count > size || offset + count < offset)
     return fail(QAOA_E_RANGE, "amplitude range out of bounds");
   if (count && !src) return fail(QAOA_E_INVALID, "null source");
-  if (!c->complemented) {
+  const uint64_t m = c->g.cmask & local_mask(c);
+  if (m == 0) {
     CUDA_TRY(cudaMemcpyAsync(c->amps + offset, src, count * sizeof(double2),
                              cudaMemcpyHostToDevice, c->stream));
-  } else {  // true index x lives at ~x: reverse the chunk
+  } else if (m == local_mask(c)) {  // true index x lives at ~x: reverse the chunk
     std::vector<double2> tmp(count);
     const double2* s2 = (const double2*)src;
     for (uint64_t i = 0; i < count; ++i) tmp[count - 1 - i] = s2[i];
     CUDA_TRY(cudaMemcpyAsync(c->amps + (size - offset - count), tmp.data(), count * sizeof(double2),
                              cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  } else {  // general mask: read-modify-write the whole state
+    std::vector<double2> all(size);
+    CUDA_TRY(cudaMemcpyAsync(all.data(), c->amps, size * sizeof(double2), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const double2* s2 = (const double2*)src;
+    for (uint64_t i = 0; i < count; ++i) all[(offset + i) ^ m] = s2[i];
+    CUDA_TRY(cudaMemcpyAsync(c->amps, all.data(), size * sizeof(double2), cudaMemcpyHostToDevice,
+                             c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -409,11 +432,33 @@ int qaoa_read_amplitudes(qaoa_ctx* c, uint64_t offset, uint64_t count, double* d
   if (offset + count > size || offset + count < offset)
     return fail(QAOA_E_RANGE, "amplitude range out of bounds");
   if (count && !dst) return fail(QAOA_E_INVALID, "null destination");
-  const uint64_t src_off = c->complemented ? size - offset - count : offset;
-  CUDA_TRY(cudaMemcpyAsync(dst, c->amps + src_off, count * sizeof(double2), cudaMemcpyDeviceToHost,
-                           c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  if (c->complemented) std::reverse((double2*)dst, (double2*)dst + count);
+  const uint64_t m = c->g.cmask & local_mask(c);
+  if (m == 0 || m == local_mask(c)) {
+    const uint64_t src_off = m ? size - offset - count : offset;
+    CUDA_TRY(cudaMemcpyAsync(dst, c->amps + src_off, count * sizeof(double2),
+                             cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (m) std::reverse((double2*)dst, (double2*)dst + count);
+  } else {
+    std::vector<double2> all(size);
+    CUDA_TRY(cudaMemcpyAsync(all.data(), c->amps, size * sizeof(double2), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    permute_chunk((double2*)dst, all.data(), offset, count, m, 0);
+  }
+  return QAOA_OK;
+}
+
+int qaoa_get_cmask(qaoa_ctx* c, uint64_t* out) {
+  if (!c || !out) return fail(QAOA_E_INVALID, "null argument");
+  *out = c->g.cmask;
+  return QAOA_OK;
+}
+
+int qaoa_set_cmask(qaoa_ctx* c, uint64_t cmask) {
+  if (!c) return fail(QAOA_E_INVALID, "null context");
+  c->g.cmask = cmask;
+  c->expect_valid = false;
   return QAOA_OK;
 }
 
@@ -480,6 +525,49 @@ int qaoa_apply_mixer(qaoa_ctx* c, double cs, double sn) {
   return QAOA_OK;
 }
 
+int qaoa_apply_rx_range(qaoa_ctx* c, int q0, int count, double cs, double sn, int flags) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (count < 1 || q0 < 0 || q0 + count > c->n)
+    return fail(QAOA_E_RANGE, "qubit range out of bounds");
+  const bool exact = flags & QAOA_RUN_EXACT;
+  const int carry = 12 - count;
+  const bool tiled = c->n >= 12 && count <= 9 && q0 >= carry;
+  if (!tiled) {  // per-qubit kernels, reference arithmetic
+    for (int q = q0; q < q0 + count; ++q) CUDA_TRY(launch_rx_gate(c->amps, c->n, q, cs, sn, c->stream));
+  } else {
+    SweepArgs a;
+    memset(&a, 0, sizeof(a));
+    a.amps = c->amps;
+    a.g = c->g;
+    a.ntiles = 1ll << (c->n - 12);
+    a.carry = carry;
+    a.q = q0;
+    uint32_t fl = kStage1;
+    if (exact) {
+      fl |= kExact;
+      a.rx1 = RxStage{cs, sn, 0};
+    } else {
+      std::complex<double> f;
+      if (std::fabs(cs) >= std::fabs(sn)) {
+        a.rx1 = RxStage{sn / cs, 0.0, 1};
+        f = std::pow(std::complex<double>(cs, 0.0), count);
+      } else {
+        a.rx1 = RxStage{-cs / sn, 0.0, 1};
+        f = std::pow(std::complex<double>(0.0, -sn), count);
+        c->g.cmask ^= (((1ull << count) - 1ull) << q0);
+      }
+      fl |= kScale;
+      a.scale = make_double2(f.real(), f.imag());
+    }
+    a.flags = fl;
+    CUDA_TRY(launch_sweep(a, (int)a.ntiles, c->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->expect_valid = false;
+  return QAOA_OK;
+}
+
 int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double* cs,
                     const double* sn, int flags) {
   int rc = check_ctx(c);
@@ -512,7 +600,7 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
     if (!from_state) {
       CUDA_TRY(launch_fill(c->amps, size, make_double2(u, 0.0), c->stream));
       ++c->last_launches;
-      c->complemented = false;
+      c->g.cmask = 0;
     }
     for (int l = 0; l < p; ++l) {
       CUDA_TRY(launch_cost_gate(c->amps, size, c->g, c->d_tables + (size_t)l * tl, c->stream));
@@ -564,12 +652,12 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
     } else if (std::fabs(cs[l]) >= std::fabs(sn[l])) {
       // RX = c [[1, -i t], [-i t, 1]], t = s / c
       stages[l] = RxStage{sn[l] / cs[l], 0.0, 1};
-      prev_scale = std::pow(std::complex<double>(cs[l], 0.0), n_total);
+      prev_scale = std::pow(std::complex<double>(cs[l], 0.0), n);
     } else {
       // RX = (-i s) X [[1, i k], [i k, 1]], k = c / s: run form 1 with t = -k and
       // complement every bit (X^n) by bookkeeping instead of data movement.
       stages[l] = RxStage{-cs[l] / sn[l], 0.0, 1};
-      prev_scale = std::pow(std::complex<double>(0.0, -sn[l]), n_total);
+      prev_scale = std::pow(std::complex<double>(0.0, -sn[l]), n);
       flips ^= 1;
     }
   }
@@ -584,7 +672,7 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
 
   if (p == 0) {
     if (!from_state) {
-      c->complemented = false;
+      c->g.cmask = 0;
       CUDA_TRY(launch_fill(c->amps, size, make_double2(u, 0.0), c->stream));
       ++c->last_launches;
       c->last_bytes += 16.0 * size;
@@ -646,7 +734,8 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
     c->last_bytes += ((fl & kGen) ? 16.0 : 32.0) * (double)size;
     if ((rc = record_event(c, timing, ev++))) return rc;
   }
-  c->complemented = (from_state ? c->complemented : false) ^ (flips != 0);
+  if (!from_state) c->g.cmask = 0;
+  if (flips) c->g.cmask ^= local_mask(c);
   if (want_expect) {
     if ((rc = reduce_to_host(c, grid, 0, &c->expect_value))) return rc;
     ++c->last_launches;
@@ -704,7 +793,7 @@ int qaoa_max_abs_diff(qaoa_ctx* a, qaoa_ctx* b, double* out) {
   CUDA_TRY(cudaStreamSynchronize(b->stream));
   const int grid = reduce_grid();
   if ((rc = ensure_partials(a, grid))) return rc;
-  const uint64_t xmask = (a->complemented != b->complemented) ? (1ull << a->n) - 1ull : 0ull;
+  const uint64_t xmask = (a->g.cmask ^ b->g.cmask) & local_mask(a);
   CUDA_TRY(launch_max_abs_diff(a->amps, b->amps, 1ull << a->n, xmask, a->partials, grid, a->stream));
   return reduce_to_host(a, grid, 1, out);
 }
@@ -724,7 +813,9 @@ int qaoa_build_cut_table(qaoa_ctx* c) {
     }
     c->cut_bytes = bytes_per;
   }
-  CUDA_TRY(launch_cut_table(c->cut_table, bytes_per, c->n, c->g, c->stream));
+  GraphDev gt = c->g;
+  gt.cmask = 0;  // the table is of true indices, independent of the state
+  CUDA_TRY(launch_cut_table(c->cut_table, bytes_per, c->n, gt, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   return QAOA_OK;
 }

@@ -14,10 +14,14 @@ constexpr int kMaxNodes = 64;  // graph.py:15 MASK_BITS
 // Graph in physical bit positions.  rm[i]: row mask (edges (i, j), j > i,
 // graph.py:57-59); adj[i]: full neighbour mask.  x_hi: fixed high bits of the
 // basis index (shard id for a sharded state, 0 otherwise).
+// cmask: complement mask of the stored state -- the amplitude of true basis
+// index x is stored at physical index x ^ cmask (fast-mode bookkeeping of the
+// second factored RX form, see qaoa_capi.cu); cut counts use x_hi ^ cmask ^ local.
 struct GraphDev {
   uint64_t rm[kMaxNodes];
   uint64_t adj[kMaxNodes];
   uint64_t x_hi;
+  uint64_t cmask;
   int n_nodes;
   int tot_edge;
 };
@@ -45,26 +49,27 @@ __device__ __forceinline__ int cut_count(uint64_t x, const GraphDev& g) {
 }
 
 // Cut counts of the 16 states x0 ^ (r0 << v0) ^ ... ^ (r3 << v3), r in [0, 16),
-// where bits v0..v3 of x0 are zero: C(x0) once, then per flipped node k
-// delta_k = deg(v_k) - 2 popc(adj[v_k] & x0), minus 2 for every edge between
-// two flipped nodes.  Bit-exact integer arithmetic.
+// for any x0: C(x0) once, then per flipped node k
+//   delta_k = s_k (deg(v_k) - 2 popc(adj[v_k] & x0)),  s_k = +1 if bit v_k of x0
+// is 0 else -1, and -2 s_j s_k for every edge between two flipped nodes.
+// Bit-exact integer arithmetic.
 template <bool WIDE>
 __device__ __forceinline__ void cut_counts16(uint64_t x0, const int v[4], const GraphDev& g,
                                              int (&c)[16]) {
   const int c0 = cut_count<WIDE>(x0, g);
-  int d[4];
-  int a01, a02, a03, a12, a13, a23;
+  int d[4], sg[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const uint64_t m = g.adj[v[k]];
-    d[k] = __popcll(m) - 2 * __popcll(m & x0);
+    sg[k] = ((x0 >> v[k]) & 1ull) ? -1 : 1;
+    d[k] = sg[k] * (__popcll(m) - 2 * __popcll(m & x0));
   }
-  a01 = 2 * (int)((g.adj[v[0]] >> v[1]) & 1ull);
-  a02 = 2 * (int)((g.adj[v[0]] >> v[2]) & 1ull);
-  a03 = 2 * (int)((g.adj[v[0]] >> v[3]) & 1ull);
-  a12 = 2 * (int)((g.adj[v[1]] >> v[2]) & 1ull);
-  a13 = 2 * (int)((g.adj[v[1]] >> v[3]) & 1ull);
-  a23 = 2 * (int)((g.adj[v[2]] >> v[3]) & 1ull);
+  const int a01 = 2 * sg[0] * sg[1] * (int)((g.adj[v[0]] >> v[1]) & 1ull);
+  const int a02 = 2 * sg[0] * sg[2] * (int)((g.adj[v[0]] >> v[2]) & 1ull);
+  const int a03 = 2 * sg[0] * sg[3] * (int)((g.adj[v[0]] >> v[3]) & 1ull);
+  const int a12 = 2 * sg[1] * sg[2] * (int)((g.adj[v[1]] >> v[2]) & 1ull);
+  const int a13 = 2 * sg[1] * sg[3] * (int)((g.adj[v[1]] >> v[3]) & 1ull);
+  const int a23 = 2 * sg[2] * sg[3] * (int)((g.adj[v[2]] >> v[3]) & 1ull);
   c[0] = c0;
   c[1] = c0 + d[0];
   c[2] = c0 + d[1];

@@ -57,7 +57,7 @@ __global__ void cost_gate_kernel(double2* __restrict__ amps, int n_local, GraphD
        w += warps) {
     const uint64_t x0 = (w << 9) | (uint64_t)lane;
     int c[16];
-    cut_counts16<WIDE>(g.x_hi | x0, v, g, c);
+    cut_counts16<WIDE>((g.x_hi | x0) ^ g.cmask, v, g, c);
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       const uint64_t x = x0 | ((uint64_t)r << 5);
@@ -71,7 +71,7 @@ __global__ void cost_gate_small_kernel(double2* __restrict__ amps, uint64_t n, G
                                        const double2* __restrict__ table) {
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n;
        x += (uint64_t)gridDim.x * blockDim.x) {
-    const int c = cut_count<WIDE>(g.x_hi | x, g);
+    const int c = cut_count<WIDE>((g.x_hi | x) ^ g.cmask, g);
     amps[x] = cmul_np(amps[x], table[2 * g.tot_edge - 2 * c]);
   }
 }
@@ -128,7 +128,7 @@ __global__ void expectation_kernel(const double2* __restrict__ amps, int n_local
          w += warps) {
       const uint64_t x0 = (w << 9) | (uint64_t)lane;
       int c[16];
-      cut_counts16<WIDE>(g.x_hi | x0, v, g, c);
+      cut_counts16<WIDE>((g.x_hi | x0) ^ g.cmask, v, g, c);
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         const double2 a = __ldcs(amps + (x0 | ((uint64_t)r << 5)));
@@ -140,7 +140,7 @@ __global__ void expectation_kernel(const double2* __restrict__ amps, int n_local
     for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n;
          x += (uint64_t)gridDim.x * blockDim.x) {
       const double2 a = amps[x];
-      acc += (a.x * a.x + a.y * a.y) * (double)cut_count<WIDE>(g.x_hi | x, g);
+      acc += (a.x * a.x + a.y * a.y) * (double)cut_count<WIDE>((g.x_hi | x) ^ g.cmask, g);
     }
   }
   const double t = block_sum<kBlock>(acc, scratch);

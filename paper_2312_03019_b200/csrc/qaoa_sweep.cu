@@ -112,17 +112,23 @@ struct TileCtx {
 };
 
 // Per-tile cut-count basis, computed once per CTA by warp 0 (lane-parallel over
-// nodes): K = C(h) for the tile's non-tile bits h (tile bits zero) and, per tile
-// node k, d[k] = deg(k) - 2 popc(adj[k] & h) = change of C when node k alone
-// flips.  adjl[k] = tile-local neighbour mask of tile node k (12 bits).
+// nodes).  h = true index of tile element 0 with all tile bits cleared
+// (x_hi ^ cmask ^ base, see GraphDev::cmask); K = C(h); per tile node k,
+// d[k] = deg(k) - 2 popc(adj[k] & h) (change of C when node k alone is set);
+// adjl[k] = tile-local neighbour mask (12 bits); tmask = cmask's tile bits (the
+// true tile bits of tile index t are t ^ tmask).
 struct CutBasis {
   int K;
+  int tmask;
   int d[12];
   int adjl[12];
 };
 
 template <bool WIDE, int C>
-__device__ __forceinline__ void cut_basis(const SweepArgs& a, uint64_t h, int q, CutBasis* cb) {
+__device__ __forceinline__ void cut_basis(const SweepArgs& a, uint64_t base, int q, CutBasis* cb) {
+  const uint64_t tile_phys = (C >= 12) ? 0xFFFull
+                                       : (((1ull << C) - 1ull) | (((1ull << (12 - C)) - 1ull) << q));
+  const uint64_t h = (a.g.x_hi ^ a.g.cmask ^ base) & ~tile_phys;
   const int lane = threadIdx.x & 31;
   int part = 0;
   for (int i = lane; i < a.g.n_nodes; i += 32) {
@@ -131,6 +137,10 @@ __device__ __forceinline__ void cut_basis(const SweepArgs& a, uint64_t h, int q,
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  const uint64_t cm = a.g.cmask;
+  const int tm = (int)((C >= 12) ? (cm & 0xFFFull)
+                                 : ((cm & ((1ull << C) - 1ull)) |
+                                    (((cm >> q) & ((1ull << (12 - C)) - 1ull)) << C)));
   if (lane < 12) {
     const int p = tile_pos<C>(lane, q);
     const uint64_t m = a.g.adj[p];
@@ -139,30 +149,38 @@ __device__ __forceinline__ void cut_basis(const SweepArgs& a, uint64_t h, int q,
     const uint32_t hi = (C >= 12) ? 0u : (uint32_t)((m >> q) & ((1ull << (12 - C)) - 1ull)) << C;
     cb->adjl[lane] = (int)(lo | hi);
   }
-  if (lane == 0) cb->K = part;
+  if (lane == 0) {
+    cb->K = part;
+    cb->tmask = tm;
+  }
 }
 
-// C(x) for the 16 registers of mapping M: C(h | t) = K + sum_{k in t} d[k] - 2 E(t),
-// E(t) = edges among the set tile nodes of t.  Exact integer arithmetic.
+// C(x) for the 16 registers of mapping M.  With T = true tile bits of the
+// thread's register-0 element: C(h | T) = K + sum_{k in T} (d[k] - popc(adjl[k] & T));
+// flipping register node j changes C by s_j (d[j] - 2 popc(adjl[j] & T)) with
+// s_j = -1 if bit j of T is set, and each edge between two flipped nodes j, k
+// adds -2 s_j s_k.  Exact integer arithmetic.
 template <int M>
 __device__ __forceinline__ void cut16(const CutBasis* cb, int (&c)[16]) {
-  const int t = tile_index<M>(threadIdx.x, 0);
+  const int T = tile_index<M>(threadIdx.x, 0) ^ cb->tmask;
   constexpr int g = group_of<M>();
   int c0 = cb->K;
 #pragma unroll
-  for (int k = 0; k < 12; ++k) {
-    if (k >= 4 * g && k < 4 * g + 4) continue;  // register bits are zero in t
-    if ((t >> k) & 1) c0 += cb->d[k] - __popc(cb->adjl[k] & t);
-  }
-  int d[4], al[4];
+  for (int k = 0; k < 12; ++k)
+    if ((T >> k) & 1) c0 += cb->d[k] - __popc(cb->adjl[k] & T);
+  int d[4], al[4], sg[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     al[j] = cb->adjl[4 * g + j];
-    d[j] = cb->d[4 * g + j] - 2 * __popc(al[j] & t);
+    sg[j] = ((T >> (4 * g + j)) & 1) ? -1 : 1;
+    d[j] = sg[j] * (cb->d[4 * g + j] - 2 * __popc(al[j] & T));
   }
-  const int a01 = 2 * ((al[0] >> (4 * g + 1)) & 1), a02 = 2 * ((al[0] >> (4 * g + 2)) & 1);
-  const int a03 = 2 * ((al[0] >> (4 * g + 3)) & 1), a12 = 2 * ((al[1] >> (4 * g + 2)) & 1);
-  const int a13 = 2 * ((al[1] >> (4 * g + 3)) & 1), a23 = 2 * ((al[2] >> (4 * g + 3)) & 1);
+  const int a01 = 2 * sg[0] * sg[1] * ((al[0] >> (4 * g + 1)) & 1);
+  const int a02 = 2 * sg[0] * sg[2] * ((al[0] >> (4 * g + 2)) & 1);
+  const int a03 = 2 * sg[0] * sg[3] * ((al[0] >> (4 * g + 3)) & 1);
+  const int a12 = 2 * sg[1] * sg[2] * ((al[1] >> (4 * g + 2)) & 1);
+  const int a13 = 2 * sg[1] * sg[3] * ((al[1] >> (4 * g + 3)) & 1);
+  const int a23 = 2 * sg[2] * sg[3] * ((al[2] >> (4 * g + 3)) & 1);
   c[0] = c0;
   c[1] = c0 + d[0];
   c[2] = c0 + d[1];
@@ -291,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const SweepArgs a) {
   }
   const bool need_cut = flags & (kPreCost | kMidCost | kExpect);
   if (need_cut) {
-    if (tid < 32) cut_basis<WIDE, C>(a, a.g.x_hi | tc.base, q, &cb);
+    if (tid < 32) cut_basis<WIDE, C>(a, tc.base, q, &cb);
     __syncthreads();
   }
   const int e = a.g.tot_edge;

@@ -1,0 +1,294 @@
+"""Multi-GPU QAOA: the 2^N state sharded over G = 2^g devices by its top g
+physical qubits (the reference has no distributed state,
+SPEC.md:186).
+
+Per level l (cost_l, then RX_l on every qubit):
+  1. every shard runs the fused engine on its N-g local qubits
+     (cost_l + RX_l, ``qaoa_run_layers`` with p=1) -- shard-local;
+  2. the g global physical bits are swapped with the top g local bits
+     (one all-to-all of G equal contiguous chunks: chunk d of rank r <-> chunk r
+     of rank d; (G-1)/G of each shard crosses the links);
+  3. the g qubits that just became local get RX_l in ONE fused sweep
+     (``qaoa_apply_rx_range``).
+The permutation is kept (never swapped back): ``ShardLayout.phys`` tracks the
+physical bit of every logical qubit, the cost kernels receive the graph's row
+masks relabelled to physical positions plus the shard's fixed high bits, and
+the fast-mode complement mask is permuted with the data.  <C> = fixed-rank-order
+sum of the shard partials (deterministic).
+
+Engines and exchangers are pluggable: ``CudaShard`` (the product: one engine
+context per shard) with ``DistExchanger`` (torch.distributed, NCCL over
+NVLink on a node, gloo on CPU) or ``LocalExchanger`` (G virtual shards in one
+process, device-to-device copies) -- the tests also drive this host logic with
+a CPU shard built on the oracle.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Protocol, Sequence
+
+import numpy as np
+
+from .circuit import QaoaParams, level_arrays
+from .graph import Graph
+
+
+# --------------------------------------------------------------------------
+# qubit placement
+# --------------------------------------------------------------------------
+@dataclass
+class ShardLayout:
+    """Logical -> physical qubit placement of a state sharded 2^g ways."""
+
+    n_total: int
+    g: int
+    phys: list[int] = field(default_factory=list)
+
+    def __post_init__(self):
+        if not self.phys:
+            self.phys = list(range(self.n_total))
+        if self.g < 0 or self.g >= self.n_total:
+            raise ValueError("shard bits must be in [0, n)")
+
+    @property
+    def n_local(self) -> int:
+        return self.n_total - self.g
+
+    def swap_top(self) -> None:
+        """Global physical bits n_local+k <-> local physical bits n_local-g+k."""
+        nl, g = self.n_local, self.g
+        where = {p: q for q, p in enumerate(self.phys)}
+        for k in range(g):
+            a, b = nl - g + k, nl + k
+            qa, qb = where[a], where[b]
+            self.phys[qa], self.phys[qb] = b, a
+            where[a], where[b] = qb, qa
+
+    def swap_bits(self, x: int) -> int:
+        """Apply the same bit swap to a physical index / mask."""
+        nl, g = self.n_local, self.g
+        lo = (x >> (nl - g)) & ((1 << g) - 1)
+        hi = (x >> nl) & ((1 << g) - 1)
+        x &= ~((((1 << g) - 1) << (nl - g)) | (((1 << g) - 1) << nl))
+        return x | (hi << (nl - g)) | (lo << nl)
+
+    def physical_row_masks(self, g: Graph) -> list[int]:
+        """Row masks of the graph relabelled to physical bit positions."""
+        masks = [0] * self.n_total
+        for i, j, _ in g.edges:
+            a, b = self.phys[i], self.phys[j]
+            if a > b:
+                a, b = b, a
+            masks[a] |= 1 << b
+        return masks
+
+    def logical_to_physical(self, idx: np.ndarray) -> np.ndarray:
+        out = np.zeros_like(idx)
+        for q, p in enumerate(self.phys):
+            out |= ((idx >> np.uint64(q)) & np.uint64(1)) << np.uint64(p)
+        return out
+
+
+# --------------------------------------------------------------------------
+# shard engines
+# --------------------------------------------------------------------------
+class Shard(Protocol):
+    rank: int
+    n: int
+
+    def set_graph(self, n_nodes: int, masks: Sequence[int], tot_edge: int, x_hi: int) -> None: ...
+    def run_level(self, table: np.ndarray, c: float, s: float, first: bool) -> None: ...
+    def apply_rx_range(self, q0: int, count: int, c: float, s: float) -> None: ...
+    def get_cmask(self) -> int: ...
+    def set_cmask(self, m: int) -> None: ...
+    def expectation(self) -> float: ...
+    def tensor(self): ...
+    def synchronize(self) -> None: ...
+
+
+class CudaShard:
+    """One engine context (C ABI) holding one shard on one GPU."""
+
+    def __init__(self, n_local: int, rank: int, device: int = 0, exact: bool = False,
+                 stream: int | None = None):
+        from . import _lib
+        from .state import Engine
+
+        self._lib = _lib
+        self.rank = rank
+        self.n = n_local
+        self.device = device
+        self.exact = exact
+        self.eng = Engine(n_local, device, stream=stream)
+
+    def set_graph(self, n_nodes, masks, tot_edge, x_hi):
+        from . import _lib
+
+        m = np.ascontiguousarray(np.array(masks, dtype=np.uint64))
+        self.eng.call("qaoa_set_graph", int(n_nodes), m.ctypes.data_as(_lib._u64p), int(tot_edge),
+                      int(x_hi))
+
+    def run_level(self, table, c, s, first):
+        from . import _lib
+
+        t = np.ascontiguousarray(table, dtype=np.complex128)
+        cs = np.array([c], dtype=np.float64)
+        ss = np.array([s], dtype=np.float64)
+        flags = (0 if first else _lib.RUN_FROM_STATE) | (_lib.RUN_EXACT if self.exact else 0)
+        self.eng.call("qaoa_run_layers", 1, _lib.dptr(t.view(np.float64)), _lib.dptr(cs),
+                      _lib.dptr(ss), flags)
+
+    def apply_rx_range(self, q0, count, c, s):
+        from . import _lib
+
+        self.eng.call("qaoa_apply_rx_range", int(q0), int(count), float(c), float(s),
+                      _lib.RUN_EXACT if self.exact else 0)
+
+    def get_cmask(self) -> int:
+        import ctypes
+
+        out = ctypes.c_uint64()
+        self.eng.call("qaoa_get_cmask", ctypes.byref(out))
+        return int(out.value)
+
+    def set_cmask(self, m: int) -> None:
+        self.eng.call("qaoa_set_cmask", int(m))
+
+    def expectation(self) -> float:
+        return self.eng.scalar("qaoa_expectation")
+
+    def tensor(self):
+        from .state import _wrap_device
+        import torch
+
+        return _wrap_device(self.eng.state_ptr(), 16 << self.n, self.device).view(torch.complex128)
+
+    def synchronize(self):
+        self.eng.call("qaoa_synchronize")
+
+    def close(self):
+        self.eng.close()
+
+
+# --------------------------------------------------------------------------
+# exchangers: swap chunk d of shard r with chunk r of shard d (all r != d)
+# --------------------------------------------------------------------------
+class LocalExchanger:
+    """All shards live in this process (virtual shards): pairwise chunk swaps."""
+
+    def __init__(self, shards: Sequence[Shard]):
+        self.shards = list(shards)
+
+    def exchange(self, g: int) -> None:
+        import torch
+
+        G = len(self.shards)
+        ts = [s.tensor() for s in self.shards]
+        chunk = ts[0].numel() // G
+        for s in self.shards:
+            s.synchronize()
+        for r in range(G):
+            for d in range(r + 1, G):
+                a = ts[r][d * chunk:(d + 1) * chunk]
+                b = ts[d][r * chunk:(r + 1) * chunk]
+                tmp = a.clone()
+                a.copy_(b)
+                b.copy_(tmp)
+        if ts[0].is_cuda:
+            torch.cuda.synchronize(ts[0].device)
+
+
+class DistExchanger:
+    """One shard per process; torch.distributed point-to-point in pieces of
+    ``piece_elems`` amplitudes through a staging buffer (the in-place swap needs
+    no second shard-sized buffer: a 128 GiB shard at N=36, G=8 leaves no room)."""
+
+    def __init__(self, shard: Shard, rank: int, world: int, piece_elems: int = 1 << 24,
+                 group=None):
+        self.shard = shard
+        self.rank = rank
+        self.world = world
+        self.piece = piece_elems
+        self.group = group
+        self.staging = None
+
+    def exchange(self, g: int) -> None:
+        import torch
+        import torch.distributed as dist
+
+        G, r = self.world, self.rank
+        t = torch.view_as_real(self.shard.tensor())  # [2^n, 2] float64 (NCCL has no c128)
+        chunk = t.shape[0] // G
+        piece = min(self.piece, chunk)
+        peers = [d for d in range(G) if d != r]
+        if self.staging is None or self.staging.shape[0] < piece * len(peers):
+            self.staging = torch.empty((piece * len(peers), 2), dtype=t.dtype, device=t.device)
+        self.shard.synchronize()
+        for off in range(0, chunk, piece):
+            ln = min(piece, chunk - off)
+            ops = []
+            for k, d in enumerate(peers):
+                ops.append(dist.P2POp(dist.isend, t[d * chunk + off: d * chunk + off + ln], d,
+                                      group=self.group))
+                ops.append(dist.P2POp(dist.irecv, self.staging[k * piece: k * piece + ln], d,
+                                      group=self.group))
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+            for k, d in enumerate(peers):
+                t[d * chunk + off: d * chunk + off + ln].copy_(self.staging[k * piece: k * piece + ln])
+        if t.is_cuda:
+            torch.cuda.synchronize(t.device)
+
+
+# --------------------------------------------------------------------------
+# the sharded circuit
+# --------------------------------------------------------------------------
+def simulate_sharded(g: Graph, params: QaoaParams, shards: Sequence[Shard], exchanger,
+                     g_bits: int, layout: ShardLayout | None = None) -> ShardLayout:
+    """Run the p-level circuit on a state sharded 2^g_bits ways.  ``shards`` are
+    the shards owned by this process (all G for virtual shards, one per rank
+    under torch.distributed).  Returns the final qubit layout."""
+    n_total = g.n
+    layout = layout or ShardLayout(n_total, g_bits)
+    nl = layout.n_local
+    if g_bits > 9 or nl - g_bits < 0:
+        raise ValueError("unsupported shard count")
+    tables, cs, ss = level_arrays(g, params)
+
+    def push_graph():
+        masks = layout.physical_row_masks(g)
+        for sh in shards:
+            sh.set_graph(n_total, masks, g.tot_edge, sh.rank << nl)
+
+    push_graph()
+    for lvl in range(params.p):
+        for sh in shards:
+            sh.run_level(tables[lvl], float(cs[lvl]), float(ss[lvl]), first=(lvl == 0))
+        if g_bits == 0:
+            continue
+        exchanger.exchange(g_bits)
+        for sh in shards:
+            sh.set_cmask(layout.swap_bits(sh.get_cmask()))
+        layout.swap_top()
+        push_graph()
+        for sh in shards:
+            sh.apply_rx_range(nl - g_bits, g_bits, float(cs[lvl]), float(ss[lvl]))
+    return layout
+
+
+def sharded_expectation(shards: Sequence[Shard], world_sum=None) -> float:
+    """Deterministic <C>: shard partials summed in rank order."""
+    parts = {sh.rank: sh.expectation() for sh in shards}
+    if world_sum is not None:
+        parts = world_sum(parts)
+    return float(sum(parts[r] for r in sorted(parts)))
+
+
+def gather_true_state(layout: ShardLayout, stored: np.ndarray, cmask: int) -> np.ndarray:
+    """Host reassembly for tests: stored = concatenation of the shards in rank
+    order (physical index = rank << n_local | local).  Returns the state in
+    logical order: true[X] = stored[phys(X) ^ cmask]."""
+    idx = np.arange(stored.size, dtype=np.uint64)
+    return stored[layout.logical_to_physical(idx) ^ np.uint64(cmask)]
