@@ -12,9 +12,11 @@ needed between steps.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--n 30] [--p 10] [--exact]
 
-N > 1 (one process per GPU via torch.distributed.run): every rank runs its own
-full N-qubit state (weak scaling, "replicas": the sharded multi-GPU engine is
-exercised by its own tests).  Device time is the max over ranks.
+N > 1 (one process per GPU via torch.distributed.run, NCCL): the same N=30
+state is sharded over the G ranks by its top log2(G) qubits (strong scaling,
+paper_2312_03019_b200.sharded: shard-local fused sweeps + one global<->local
+chunk exchange per level).  ``--replicas`` instead runs one full state per rank
+(weak scaling).  Device time is the max over ranks.
 
 ``--impl reference`` times the CPU oracle (oracle/, a C restatement of the
 reference's algorithm, bit-exact with it) on all host threads: each step is one
@@ -193,6 +195,76 @@ def run_reference(args, rank: int, world: int):
     return 0
 
 
+def run_sharded(args, rank: int, world: int, local: int):
+    """Strong scaling: one N-qubit state sharded over `world` GPUs (NCCL)."""
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2312_03019_b200 as Q
+    from paper_2312_03019_b200.sharded import CudaShard, DistExchanger, simulate_sharded
+
+    if world & (world - 1):
+        raise SystemExit("sharded mode needs a power-of-two GPU count")
+    dist = init_dist(world, local)
+    torch.cuda.set_device(local)
+    n, p = args.n, args.p
+    gbits = world.bit_length() - 1
+    g = Q.random_regular_graph(n, 3, seed=0)
+    params = Q.params_from_seed(p, 0)
+    shard = CudaShard(n - gbits, rank, device=local, exact=args.exact,
+                      stream=torch.cuda.current_stream(local).cuda_stream)
+    exch = DistExchanger(shard, rank, world)
+
+    def step():
+        simulate_sharded(g, params, [shard], exch, gbits)
+        part = torch.tensor([shard.expectation()], dtype=torch.float64, device=f"cuda:{local}")
+        allp = [torch.zeros_like(part) for _ in range(world)]
+        tdist.all_gather(allp, part)
+        return float(sum(t.item() for t in allp))  # rank order: deterministic
+
+    for _ in range(max(args.warmup, 3)):
+        val = step()
+    dist.barrier()
+    torch.cuda.synchronize(local)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record()
+        for _ in range(args.steps):
+            val = step()
+        stop.record()
+        torch.cuda.synchronize(local)
+    dev_ms = start.elapsed_time(stop)
+    t = torch.tensor([dev_ms], device=f"cuda:{local}")
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    dev_ms = float(t.item())
+    layers = p * args.steps / (dev_ms * 1e-3)
+    per_level = (n + 1) * (1 << n)
+    xbytes = (world - 1) / world * 16 * (1 << (n - gbits))  # per rank per direction per level
+    if rank == 0:
+        peak, peak_kind = measured_peaks()
+        line = {
+            "metric": METRIC, "value": layers, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic",
+            "config": {"workload": f"u3r N={n} seed 0, p={p} levels, complex128 (BASELINE configs[2])",
+                       "n_qubits": n, "p": p, "parallelism": f"state sharded over {world} GPUs "
+                       f"(top {gbits} qubits), NCCL P2P exchange",
+                       "l2": "no flush: shards >> L2"},
+            "amp_updates_per_s": layers * per_level, "expectation": val,
+            "nvlink": {"bytes_per_level_per_rank_per_direction": xbytes,
+                       "peak_GBps_per_direction": 770.0},
+            "roofline": {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s",
+                         "frac": None, "traffic": None, "peak_kind": peak_kind},
+            "cpu_baseline": None, "e2e": None,
+            "gpu_launches": None, "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    shard.close()
+    dist.destroy_process_group()
+    return 0
+
+
 def run_ours(args, rank: int, world: int, local: int):
     import torch
 
@@ -340,10 +412,14 @@ def main():
     ap.add_argument("--exact", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: one full state per rank (weak scaling) instead of sharding")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if world > 1 and not args.replicas:
+        return run_sharded(args, rank, world, local)
     return run_ours(args, rank, world, local)
 
 

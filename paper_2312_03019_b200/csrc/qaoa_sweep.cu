@@ -7,15 +7,16 @@
 // amplitudes, C >= 3 -> >= 128 B) and bits q..q+11-C (the qubits mixed by this
 // sweep).  The low sweep has C = 12 (tile = 4096 consecutive amplitudes).
 //
-// A persistent CTA of 256 threads holds one tile in registers, 16 amplitudes
+// A CTA of 256 threads (two per SM) holds one tile in registers, 16 amplitudes
 // per thread, and re-maps it through shared memory between three register
 // groups of four tile bits:
 //   M2: registers = tile bits 8..11, threads = tile bits 0..7        (HBM load/store)
 //   M0: registers = tile bits 0..3,  threads = tile bits 4..11
 //   M1: registers = tile bits 4..7,  threads = tile bits 0..3, 8..11 (HBM store)
 // RX butterflies on register bits are register-local; tile bit 3 is lane bit 3
-// in both M2 and M1, so a lone active bit there is done with warp shuffles
-// instead of an extra shared-memory pass.  The diagonal cost phase (lookup of
+// in both M2 and M1, so a lone mixed bit there (C = 3) is traded into a
+// register bit by a half-data warp-shuffle transpose instead of an extra
+// shared-memory pass.  The diagonal cost phase (lookup of
 // exp(-i gamma (E - 2C)/2) by the integer cut count C(x), recomputed from the
 // row masks -- the cut table is never read from HBM), the fast-mode scale and
 // the <C> reduction are applied on the registers between / after the stages.
@@ -41,15 +42,17 @@ constexpr int kRegs = 16;
 constexpr int kSlots = kTile + kTile / 16;
 __host__ __device__ constexpr int slot(int t) { return t + (t >> 4); }
 
-// Tile index of register r of thread tid in mapping M.
+// Tile index of register r of thread tid in mapping M.  M3 / M4 are M2 / M1
+// after lane bit 3 and register bit 0 traded places (transpose_lane3): register
+// bit 0 then holds tile bit 3 and lane bit 3 holds tile bit 8 (M3) / 4 (M4).
 template <int M>
 __host__ __device__ constexpr int tile_index(int tid, int r) {
   return M == 2 ? (tid | (r << 8))
-                : (M == 0 ? ((tid << 4) | r) : ((tid & 15) | ((tid >> 4) << 8) | (r << 4)));
-}
-template <int M>
-__host__ __device__ constexpr int slot_stride() {
-  return M == 2 ? 272 : (M == 0 ? 1 : 17);
+       : M == 0 ? ((tid << 4) | r)
+       : M == 1 ? ((tid & 15) | ((tid >> 4) << 8) | (r << 4))
+       : M == 3 ? ((tid & 0xF7) | (((tid >> 3) & 1) << 8) | ((r & 1) << 3) | ((r >> 1) << 9))
+                : ((tid & 7) | (((tid >> 3) & 1) << 4) | ((tid >> 4) << 8) | ((r & 1) << 3) |
+                   ((r >> 1) << 5));
 }
 template <int M>
 __host__ __device__ constexpr int group_of() {
@@ -67,19 +70,22 @@ __device__ __forceinline__ int tile_pos(int k, int q) {  // physical bit of tile
   return (C >= 12 || k < C) ? k : q + (k - C);
 }
 
+// slot(thread part | register part) = slot(thread part) + slot(register part)
+// for every mapping (their low four bits never carry), so register offsets are
+// compile-time constants.
 template <int M>
 __device__ __forceinline__ void smem_store(double2* buf, int sb, const double2 (&v)[kRegs]) {
 #pragma unroll
-  for (int r = 0; r < kRegs; ++r) buf[sb + r * slot_stride<M>()] = v[r];
+  for (int r = 0; r < kRegs; ++r) buf[sb + slot(tile_index<M>(0, r))] = v[r];
 }
 template <int M>
 __device__ __forceinline__ void smem_load(const double2* buf, int sb, double2 (&v)[kRegs]) {
 #pragma unroll
-  for (int r = 0; r < kRegs; ++r) v[r] = buf[sb + r * slot_stride<M>()];
+  for (int r = 0; r < kRegs; ++r) v[r] = buf[sb + slot(tile_index<M>(0, r))];
 }
 
 struct ThreadSlots {
-  int s0, s1, s2;
+  int s[5];
 };
 
 // Re-map registers from mapping A to mapping B through shared memory.  In a
@@ -88,9 +94,26 @@ struct ThreadSlots {
 // before the first write of the next tile.
 template <int A, int B>
 __device__ __forceinline__ void exchange(double2* buf, const ThreadSlots& ts, double2 (&v)[kRegs]) {
-  smem_store<A>(buf, A == 0 ? ts.s0 : (A == 1 ? ts.s1 : ts.s2), v);
+  smem_store<A>(buf, ts.s[A], v);
   __syncthreads();
-  smem_load<B>(buf, B == 0 ? ts.s0 : (B == 1 ? ts.s1 : ts.s2), v);
+  smem_load<B>(buf, ts.s[B], v);
+}
+
+// Trade lane bit 3 for register bit 0 inside each warp: the lane with lane bit
+// 3 = 0 gives away its odd registers and receives the partner's even ones.  Half
+// the data crosses lanes (one shuffle per moved word, vs two-way for a lane
+// butterfly); afterwards tile bit 3 is a register bit (mappings M3 / M4).
+__device__ __forceinline__ void transpose_lane3(double2 (&v)[kRegs]) {
+  const bool hi = (threadIdx.x & 8) != 0;
+#pragma unroll
+  for (int r = 0; r < kRegs; r += 2) {
+    const double2 snd = hi ? v[r] : v[r + 1];
+    double2 rcv;
+    rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, 8);
+    rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, 8);
+    if (hi) v[r] = rcv;
+    else v[r + 1] = rcv;
+  }
 }
 
 // Compile-time description of which tile bits a sweep mixes: bits C..11 (C<12)
@@ -237,25 +260,6 @@ __device__ __forceinline__ void rx_regs2(double2 (&v)[kRegs], double c_or_t, dou
   }
 }
 
-template <bool EXACT>
-__device__ __forceinline__ void rx_lane3(double2 (&v)[kRegs], double c_or_t, double s) {
-#pragma unroll
-  for (int r = 0; r < kRegs; ++r) {
-    double2 o;
-    o.x = __shfl_xor_sync(0xffffffffu, v[r].x, 8);
-    o.y = __shfl_xor_sync(0xffffffffu, v[r].y, 8);
-    if (EXACT) {
-      const double nr = __dadd_rn(__dmul_rn(c_or_t, v[r].x), __dmul_rn(s, o.y));
-      const double ni = __dadd_rn(__dmul_rn(c_or_t, v[r].y), __dmul_rn(-s, o.x));
-      v[r].x = nr; v[r].y = ni;
-    } else {
-      const double nr = __fma_rn(c_or_t, o.y, v[r].x);
-      const double ni = __fma_rn(-c_or_t, o.x, v[r].y);
-      v[r].x = nr; v[r].y = ni;
-    }
-  }
-}
-
 template <int C, int M>
 __device__ __forceinline__ void store_tile(double2* __restrict__ amps, const TileCtx& tc,
                                            uint64_t Q, const double2 (&v)[kRegs]) {
@@ -293,9 +297,11 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const SweepArgs a) {
   tc.tb2 = tile_off<C>(tile_index<2>(tid, 0), Q);
   tc.tb1 = tile_off<C>(tile_index<1>(tid, 0), Q);
   ThreadSlots ts;
-  ts.s2 = slot(tile_index<2>(tid, 0));
-  ts.s1 = slot(tile_index<1>(tid, 0));
-  ts.s0 = slot(tile_index<0>(tid, 0));
+  ts.s[0] = slot(tile_index<0>(tid, 0));
+  ts.s[1] = slot(tile_index<1>(tid, 0));
+  ts.s[2] = slot(tile_index<2>(tid, 0));
+  ts.s[3] = slot(tile_index<3>(tid, 0));
+  ts.s[4] = slot(tile_index<4>(tid, 0));
   double2* __restrict__ amps = a.amps;
 
   double2 v[kRegs];
@@ -325,8 +331,13 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const SweepArgs a) {
       exchange<0, 1>(buf, ts, v);
       rx_regs2<A::g1, true>(v, r1a, r1b);
       exchange<1, 2>(buf, ts, v);
+    } else if (A::g0_shfl) {  // tile bit 3 via the lane/register transpose
+      transpose_lane3(v);
+      rx_regs2<1u, true>(v, r1a, r1b);
+      exchange<3, 1>(buf, ts, v);
+      rx_regs2<A::g1, true>(v, r1a, r1b);
+      exchange<1, 2>(buf, ts, v);
     } else {
-      if (A::g0_shfl) rx_lane3<true>(v, r1a, r1b);
       if (A::g1) {
         exchange<2, 1>(buf, ts, v);
         rx_regs2<A::g1, true>(v, r1a, r1b);
@@ -366,24 +377,34 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const SweepArgs a) {
       store_tile<C, 1>(amps, tc, Q, v);
     }
   } else {
-    // ---- fast, high set: G2 (+ lane bit 3), G1 [, cost, G1 (+ lane bit 3), G2]
+    // ---- fast, high set: G2 (+ tile bit 3), G1 [, cost, G1 (+ tile bit 3), G2]
     if (flags & kPreCost) apply_cost<2>(v, &cb, a.table, e);
     rx_regs2<A::g2, false>(v, r1a, 0.0);
-    if (A::g0_shfl) rx_lane3<false>(v, r1a, 0.0);
-    if (A::g1) {
+    if (A::g0_shfl) {  // C = 3: tile bit 3 traded into register bit 0 (M2 -> M3)
+      transpose_lane3(v);
+      rx_regs2<1u, false>(v, r1a, 0.0);
+      exchange<3, 1>(buf, ts, v);
+      rx_regs2<A::g1, false>(v, r1a, 0.0);
+      if (FLOW == 2) {
+        apply_cost<1>(v, &cb, a.table2, e);
+        rx_regs2<A::g1, false>(v, r2a, 0.0);
+        transpose_lane3(v);  // M1 -> M4
+        rx_regs2<1u, false>(v, r2a, 0.0);
+        exchange<4, 2>(buf, ts, v);
+        rx_regs2<A::g2, false>(v, r2a, 0.0);
+      }
+    } else if (A::g1) {
       exchange<2, 1>(buf, ts, v);
       rx_regs2<A::g1, false>(v, r1a, 0.0);
       if (FLOW == 2) {
         apply_cost<1>(v, &cb, a.table2, e);
         rx_regs2<A::g1, false>(v, r2a, 0.0);
-        if (A::g0_shfl) rx_lane3<false>(v, r2a, 0.0);
         exchange<1, 2>(buf, ts, v);
         rx_regs2<A::g2, false>(v, r2a, 0.0);
       }
     } else if (FLOW == 2) {
       apply_cost<2>(v, &cb, a.table2, e);
       rx_regs2<A::g2, false>(v, r2a, 0.0);
-      if (A::g0_shfl) rx_lane3<false>(v, r2a, 0.0);
     }
     constexpr int last = (A::g1 && FLOW == 1) ? 1 : 2;
     if (flags & kScale) {
