@@ -15,7 +15,7 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(_HERE, "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libqaoa_b200.so")
+LIB_PATH = os.environ.get("QAOA_B200_LIB") or os.path.join(LIB_DIR, "libqaoa_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "qaoa_b200.h")
 
