@@ -182,8 +182,8 @@ def run_reference(args, rank: int, world: int):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * p / layers, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": f"u3r N={n} seed 0, p={p} levels, complex128 (BASELINE configs[2])",
-                   "n_qubits": n, "p": p, "graph": "random 3-regular seed 0",
+        "config": {"workload": workload_name(args),
+                   "n_qubits": n, "p": p, "graph": args.graph,
                    "l2": "state >> L2 (16 GiB)"},
         "amp_updates_per_s": rate,
         "cpu_baseline": {"value": layers, "unit": UNIT, "cores": threads, "kind": "port",
@@ -193,6 +193,20 @@ def run_reference(args, rank: int, world: int):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def make_graph(Q, args):
+    if args.graph == "er":
+        return Q.erdos_renyi_graph(args.n, 0.5, seed=0)
+    return Q.random_regular_graph(args.n, 3, seed=0)
+
+
+def workload_name(args) -> str:
+    gname = "u3r" if args.graph == "u3r" else "ER(0.5)"
+    cfg = {("u3r", 30, 10): "BASELINE configs[2]", ("er", 33, 4): "BASELINE configs[3]",
+           ("u3r", 26, 4): "BASELINE configs[1]", ("u3r", 20, 1): "BASELINE configs[0]"}
+    tag = cfg.get((args.graph, args.n, args.p), "custom")
+    return f"{gname} N={args.n} seed 0, p={args.p} levels, complex128 ({tag})"
 
 
 def run_sharded(args, rank: int, world: int, local: int):
@@ -209,7 +223,7 @@ def run_sharded(args, rank: int, world: int, local: int):
     torch.cuda.set_device(local)
     n, p = args.n, args.p
     gbits = world.bit_length() - 1
-    g = Q.random_regular_graph(n, 3, seed=0)
+    g = make_graph(Q, args)
     params = Q.params_from_seed(p, 0)
     shard = CudaShard(n - gbits, rank, device=local, exact=args.exact,
                       stream=torch.cuda.current_stream(local).cuda_stream)
@@ -247,8 +261,8 @@ def run_sharded(args, rank: int, world: int, local: int):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic",
-            "config": {"workload": f"u3r N={n} seed 0, p={p} levels, complex128 (BASELINE configs[2])",
-                       "n_qubits": n, "p": p, "parallelism": f"state sharded over {world} GPUs "
+            "config": {"workload": workload_name(args),
+                       "n_qubits": n, "p": p, "graph": args.graph, "parallelism": f"state sharded over {world} GPUs "
                        f"(top {gbits} qubits), NCCL P2P exchange",
                        "l2": "no flush: shards >> L2"},
             "amp_updates_per_s": layers * per_level, "expectation": val,
@@ -275,11 +289,13 @@ def run_ours(args, rank: int, world: int, local: int):
     device = local if world > 1 else 0
     torch.cuda.set_device(device)
     n, p = args.n, args.p
-    g = Q.random_regular_graph(n, 3, seed=0)
+    g = make_graph(Q, args)
     params = Q.params_from_seed(p, 0)  # same RNG stream as reference bench.py:61-67
     tables, cs, ss = Q.level_arrays(g, params)
     stream = torch.cuda.Stream(device)
     eng = Q.Engine(n, device, stream=stream.cuda_stream)
+    if n > 30:
+        args.e2e_steps = min(args.e2e_steps, 2)
     eng.ensure_graph(g)
     flags = _lib.RUN_EXPECTATION | _lib.RUN_TIMING | (_lib.RUN_EXACT if args.exact else 0)
     L = _lib.load()
@@ -339,6 +355,23 @@ def run_ours(args, rank: int, world: int, local: int):
                 "level_roofline_frac_R3": (32 * 3 * (1 << n) * p / (dev_ms / args.steps * 1e-3))
                 / 1e9 / peak}
 
+    # ---- K1, the cut-table builder, timed once --------
+    cut_table = None
+    if args.cut_table:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eng.call("qaoa_build_cut_table")  # warm-up (module load, allocation)
+        torch.cuda.synchronize(device)
+        ev0.record(stream)
+        eng.call("qaoa_build_cut_table")
+        ev1.record(stream)
+        torch.cuda.synchronize(device)
+        ms = ev0.elapsed_time(ev1)
+        bpe = 1 if g.tot_edge <= 255 else 2
+        cut_table = {"ms": ms, "states_per_s": (1 << n) / (ms * 1e-3),
+                     "bytes_written": bpe << n, "GBps": (bpe << n) / (ms * 1e-3) / 1e9,
+                     "dtype": "uint8" if bpe == 1 else "uint16"}
+        eng.call("qaoa_free_cut_table")
+
     # ---- end to end through the public API: host inputs -> <C> on the host ----
     e2e = None
     if args.e2e_steps > 0:
@@ -381,13 +414,14 @@ def run_ours(args, rank: int, world: int, local: int):
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": f"u3r N={n} seed 0, p={p} levels, complex128 (BASELINE configs[2])",
-                       "n_qubits": n, "p": p, "graph": "random 3-regular seed 0",
+            "config": {"workload": workload_name(args),
+                       "n_qubits": n, "p": p, "graph": args.graph,
                        "schedule": "exact" if args.exact else "fast",
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": "no flush: 16 GiB state >> 126 MB L2"},
             "amp_updates_per_s": layers_per_s * per_level,
             "expectation": expect_val,
+            "cut_table_build": cut_table,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -408,10 +442,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=30)
+    ap.add_argument("--graph", choices=["u3r", "er"], default="u3r",
+                    help="u3r = random 3-regular seed 0 (configs 0-2, 4); er = G(n, 0.5) seed 0 "
+                         "(configs[3], the dense N=33 cut-table stress case)")
     ap.add_argument("--p", type=int, default=10)
     ap.add_argument("--exact", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cut-table", action="store_true", help="also time the K1 cut-table builder")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: one full state per rank (weak scaling) instead of sharding")
     args = ap.parse_args()
