@@ -106,6 +106,11 @@ __device__ __forceinline__ void exchange(double2* buf, const ThreadSlots& ts, do
 // the data crosses lanes (one shuffle per moved word, vs two-way for a lane
 // butterfly); afterwards tile bit 3 is a register bit (mappings M3 / M4).
 __device__ __forceinline__ void transpose_lane3(double2 (&v)[kRegs]) {
+  // The next exchange stores in the transposed mapping, i.e. to slots the
+  // partner lane read in the last exchange: order those reads first (the data
+  // dependency through the shuffles already does; this makes it explicit for
+  // the memory model and for racecheck).
+  __syncwarp();
   const bool hi = (threadIdx.x & 8) != 0;
 #pragma unroll
   for (int r = 0; r < kRegs; r += 2) {

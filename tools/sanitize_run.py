@@ -1,0 +1,27 @@
+"""Small workload touching every kernel variant, for compute-sanitizer
+(memcheck / racecheck / synccheck) runs on the GPU box:
+    compute-sanitizer --tool racecheck python tools/sanitize_run.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+
+import paper_2312_03019_b200 as Q
+from paper_2312_03019_b200.sharded import CudaShard, LocalExchanger, simulate_sharded
+
+for n in (5, 12, 13, 15, 16, 21):
+    g = Q.random_regular_graph(n, 3, seed=n) if n % 2 == 0 else Q.erdos_renyi_graph(n, 0.3, n)
+    for exact in (True, False):
+        pr = Q.QaoaParams((0.3, 1.2, 2.2), (0.5, 2.9, 1.1))
+        s = Q.simulate(g, pr, "bitwise", exact=exact, max_qubits=30)
+        Q.expectation(g, s)
+    Q.build_cut_table(g)
+    Q.apply_mixer_layer(s, 0.3)
+    Q.apply_cost_layer(s, g, 0.4, "bitwise")
+    Q.apply_rx(s, n - 1, 0.2)
+g = Q.random_regular_graph(16, 3, seed=1)
+shards = [CudaShard(14, r) for r in range(4)]
+simulate_sharded(g, Q.QaoaParams((0.3, 1.0), (2.9, 0.4)), shards, LocalExchanger(shards), 2)
+print("sanitize workload done")
