@@ -135,6 +135,17 @@ QAOA_API int qaoa_run_layers(qaoa_ctx* ctx, int p, const double* phase_tables, c
  * has not changed since, else runs a read-only reduction. */
 QAOA_API int qaoa_expectation(qaoa_ctx* ctx, double* out);
 
+/* Weighted graphs (the reference's "compressed" backend, cost.py:77-86,
+ * :147-159): edge list (i, j, w) in the graph's edge order (Graph.edges,
+ * graph.py:34-66).  qaoa_apply_cost_weighted multiplies by
+ * exp(-i gamma t(x) / 2), t = sum_e w_e (1 - 2 [x_i != x_j]) accumulated in edge
+ * order (bit-identical totals; the phase's sincos is within 2 ulp of glibc's).
+ * qaoa_expectation_weighted = sum_x |a_x|^2 sum_e w_e [x_i != x_j]
+ * (graph.py:144-151).  x includes x_hi / the complement mask like the integer path. */
+QAOA_API int qaoa_set_weights(qaoa_ctx* ctx, int m, const int* ei, const int* ej, const double* w);
+QAOA_API int qaoa_apply_cost_weighted(qaoa_ctx* ctx, double gamma);
+QAOA_API int qaoa_expectation_weighted(qaoa_ctx* ctx, double* out);
+
 /* Partial sum of |amp|^2 over the local shard (StateVector.norm, state.py:50-51). */
 QAOA_API int qaoa_norm_sq(qaoa_ctx* ctx, double* out);
 

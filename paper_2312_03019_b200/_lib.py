@@ -63,6 +63,9 @@ SIGNATURES = {
     "qaoa_get_cmask": (_c_int, [_vp, _u64p]),
     "qaoa_set_cmask": (_c_int, [_vp, _u64]),
     "qaoa_expectation": (_c_int, [_vp, _dp]),
+    "qaoa_set_weights": (_c_int, [_vp, _c_int, _ip, _ip, _dp]),
+    "qaoa_apply_cost_weighted": (_c_int, [_vp, _c_dbl]),
+    "qaoa_expectation_weighted": (_c_int, [_vp, _dp]),
     "qaoa_norm_sq": (_c_int, [_vp, _dp]),
     "qaoa_max_abs_diff": (_c_int, [_vp, _vp, _dp]),
     "qaoa_build_cut_table": (_c_int, [_vp]),

@@ -71,13 +71,6 @@ def validate_backend(backend: str, g: Graph | None = None) -> str:
     return backend
 
 
-def _require_engine_graph(g: Graph, what: str) -> None:
-    if not g.is_unweighted:
-        raise NotImplementedError(
-            f"{what}: the B200 engine implements the unweighted (bitwise) path; "
-            "weighted graphs are outside this build's scope")
-
-
 def rx_coefficients(beta: float) -> tuple[float, float]:
     """(cos(theta/2), sin(theta/2)) with theta = -beta (circuit.py:93, state.py:114-115)."""
     theta = -beta
@@ -116,10 +109,11 @@ def apply_cost_layer(s: StateVector, g: Graph, gamma: float, backend: str = "bas
                      use_table_popcount: bool = False) -> StateVector:
     """One cost layer, one device pass (circuit.py:65-86)."""
     validate_backend(backend, g)
-    _require_engine_graph(g, "apply_cost_layer")
-    from .cost import apply_cost_batched, apply_cost_bitwise
+    from .cost import apply_cost_batched, apply_cost_bitwise, apply_cost_compressed
 
     plan = plan_for(g)
+    if not g.is_unweighted:
+        return apply_cost_compressed(s, plan, gamma, threads)
     if batch_width is not None and backend == "bitwise":
         return apply_cost_batched(s, plan, gamma, batch_width, use_table_popcount)
     return apply_cost_bitwise(s, plan, gamma, threads)
@@ -155,11 +149,14 @@ def simulate(
 
     Extra keyword-only knobs: ``exact`` (bit-exact reference schedule),
     ``device``, ``fuse_expectation`` (accumulate <C> in the last sweep) and
-    ``state`` (reuse a StateVector's device buffer instead of allocating)."""
+    ``state`` (reuse a StateVector's device buffer instead of allocating).
+
+    Weighted graphs (backends "compressed" / "baseline") run the compressed
+    weighted cost pass (cost.py:147-159) + the mixer sweeps per level: one more
+    HBM pass per level than the fused unweighted path."""
     validate_backend(backend, g)
     if batch_width is not None and batch_width not in (1, 2, 4, 8):
         raise ValueError(f"batch width must be 1, 2, 4, or 8, got {batch_width}")
-    _require_engine_graph(g, "simulate")
     check_qubit_budget(g.n, max_qubits)
     if state is not None and state.n == g.n:
         eng = state._eng if state._eng is not None else Engine(g.n, device)
@@ -169,6 +166,15 @@ def simulate(
         eng = Engine(g.n, device)
         s = StateVector(g.n, engine=eng)
     eng.ensure_graph(g)
+    if not g.is_unweighted:
+        eng.call("qaoa_init_uniform")
+        eng.ensure_weights(g)
+        for gamma, beta in zip(params.gamma, params.beta):
+            eng.call("qaoa_apply_cost_weighted", float(gamma))
+            c, sn = rx_coefficients(beta)
+            eng.call("qaoa_apply_mixer", c, sn)
+        write_counter.add((1 << g.n) * (1 + params.p * (g.n + 1)))
+        return s
     tables, cs, ss = level_arrays(g, params)
     flags = (_lib.RUN_EXACT if exact else 0) | (_lib.RUN_EXPECTATION if fuse_expectation else 0)
     eng.call("qaoa_run_layers", params.p, _lib.dptr(tables.view(np.float64)), _lib.dptr(cs),
@@ -182,9 +188,11 @@ def expectation(g: Graph, s: StateVector) -> float:
     fixed-order reduction; the fused value of the last simulate when valid."""
     if s.n != g.n:
         raise ValueError(f"state has {s.n} qubits but graph has {g.n} nodes")
-    _require_engine_graph(g, "expectation")
     eng = s.engine()
     eng.ensure_graph(g)
+    if not g.is_unweighted:  # float cut values, graph.py:144-151
+        eng.ensure_weights(g)
+        return eng.scalar("qaoa_expectation_weighted")
     return eng.scalar("qaoa_expectation")
 
 

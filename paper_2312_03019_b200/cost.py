@@ -133,6 +133,22 @@ def apply_cost_bitwise(s: StateVector, plan: CompressedCostPlan, gamma: float,
     return s
 
 
+def apply_cost_compressed(s: StateVector, plan: CompressedCostPlan, gamma: float,
+                          threads: int = 1) -> StateVector:
+    """Weighted rotation-compressed cost layer, one device pass (cost.py:147-159):
+    amp *= exp(-i gamma t(x) / 2) with t accumulated in edge order.  Unweighted
+    graphs take the bit-exact integer path (same values, test_cost.py:153-162)."""
+    _check_state(s, plan)
+    if plan.graph.is_unweighted:
+        return apply_cost_bitwise(s, plan, gamma, threads)
+    eng = s.engine()
+    eng.ensure_graph(plan.graph)
+    eng.ensure_weights(plan.graph)
+    eng.call("qaoa_apply_cost_weighted", float(gamma))
+    write_counter.add(1 << s.n)
+    return s
+
+
 def apply_cost_batched(s: StateVector, plan: CompressedCostPlan, gamma: float, batch_width: int,
                        use_table_popcount: bool = False) -> StateVector:
     """Strip-mined variant (cost.py:179-218): the warp is the strip on the GPU, so

@@ -92,6 +92,11 @@ struct qaoa_ctx {
   // expectation cached from the last fused run
   bool expect_valid = false;
   double expect_value = 0.0;
+  // weighted edge list (compressed backend), device copies
+  int* d_ei = nullptr;
+  int* d_ej = nullptr;
+  double* d_w = nullptr;
+  int n_wedges = -1;
   // timing
   std::vector<cudaEvent_t> events;
   std::vector<float> times;
@@ -324,6 +329,9 @@ void qaoa_destroy(qaoa_ctx* c) {
   if (c->d_scalar) cudaFree(c->d_scalar);
   if (c->d_tables) cudaFree(c->d_tables);
   if (c->h_tables) cudaFreeHost(c->h_tables);
+  if (c->d_ei) cudaFree(c->d_ei);
+  if (c->d_ej) cudaFree(c->d_ej);
+  if (c->d_w) cudaFree(c->d_w);
   for (auto e : c->events) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -750,6 +758,59 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
     }
   }
   return QAOA_OK;
+}
+
+int qaoa_set_weights(qaoa_ctx* c, int m, const int* ei, const int* ej, const double* w) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (m < 0 || (m && (!ei || !ej || !w))) return fail(QAOA_E_INVALID, "bad edge list");
+  for (int e = 0; e < m; ++e)
+    if (ei[e] < 0 || ej[e] < 0 || ei[e] >= 64 || ej[e] >= 64 || ei[e] == ej[e])
+      return fail(QAOA_E_INVALID, "edge endpoint out of range");
+  if (c->d_ei) cudaFree(c->d_ei);
+  if (c->d_ej) cudaFree(c->d_ej);
+  if (c->d_w) cudaFree(c->d_w);
+  c->d_ei = nullptr;
+  c->d_ej = nullptr;
+  c->d_w = nullptr;
+  const size_t cnt = (size_t)std::max(m, 1);
+  CUDA_TRY(cudaMalloc(&c->d_ei, cnt * sizeof(int)));
+  CUDA_TRY(cudaMalloc(&c->d_ej, cnt * sizeof(int)));
+  CUDA_TRY(cudaMalloc(&c->d_w, cnt * sizeof(double)));
+  if (m) {
+    CUDA_TRY(cudaMemcpyAsync(c->d_ei, ei, m * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->d_ej, ej, m * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->d_w, w, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->n_wedges = m;
+  c->expect_valid = false;
+  return QAOA_OK;
+}
+
+int qaoa_apply_cost_weighted(qaoa_ctx* c, double gamma) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (c->n_wedges < 0) return fail(QAOA_E_STATE, "no weighted edge list set");
+  const uint64_t xbase = c->g.x_hi ^ c->g.cmask;
+  CUDA_TRY(launch_cost_weighted(c->amps, 1ull << c->n, xbase, c->d_ei, c->d_ej, c->d_w,
+                                c->n_wedges, gamma, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->expect_valid = false;
+  return QAOA_OK;
+}
+
+int qaoa_expectation_weighted(qaoa_ctx* c, double* out) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (!out) return fail(QAOA_E_INVALID, "null output");
+  if (c->n_wedges < 0) return fail(QAOA_E_STATE, "no weighted edge list set");
+  const int grid = reduce_grid();
+  if ((rc = ensure_partials(c, grid))) return rc;
+  const uint64_t xbase = c->g.x_hi ^ c->g.cmask;
+  CUDA_TRY(launch_expectation_weighted(c->amps, 1ull << c->n, xbase, c->d_ei, c->d_ej, c->d_w,
+                                       c->n_wedges, c->partials, grid, c->stream));
+  return reduce_to_host(c, grid, 0, out);
 }
 
 int qaoa_expectation(qaoa_ctx* c, double* out) {

@@ -154,6 +154,70 @@ cudaError_t launch_expectation(const double2* amps, int n_local, const GraphDev&
   return cudaGetLastError();
 }
 
+// ---- weighted graphs: the compressed backend (cost.py:77-86, :147-159) and the
+// float cut values of expectation (graph.py:144-151).  Totals are accumulated
+// per amplitude in the reference's edge order, so they are bit-identical to
+// rotation_totals() / cut_values_array(); the phase is (cos y, sin y) with
+// y = -(0.5 gamma) t exactly as np.exp(-0.5j * gamma * totals) forms it.
+struct EdgeList {
+  const int* ei;
+  const int* ej;
+  const double* w;
+  int m;
+};
+
+__global__ void cost_weighted_kernel(double2* __restrict__ amps, uint64_t n, uint64_t xbase,
+                                     EdgeList el, double half_gamma) {
+  for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < n;
+       y += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = xbase ^ y;
+    double t = 0.0;
+    for (int e = 0; e < el.m; ++e) {
+      const uint64_t diff = ((x >> __ldg(el.ei + e)) ^ (x >> __ldg(el.ej + e))) & 1ull;
+      t = __dadd_rn(t, __dmul_rn(__ldg(el.w + e), diff ? -1.0 : 1.0));
+    }
+    double sn, cs;
+    sincos(-__dmul_rn(half_gamma, t), &sn, &cs);
+    amps[y] = cmul_np(amps[y], make_double2(cs, sn));
+  }
+}
+
+__global__ void expectation_weighted_kernel(const double2* __restrict__ amps, uint64_t n,
+                                            uint64_t xbase, EdgeList el,
+                                            double* __restrict__ partials) {
+  __shared__ double scratch[kBlock / 32];
+  double acc = 0.0;
+  for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < n;
+       y += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = xbase ^ y;
+    double v = 0.0;
+    for (int e = 0; e < el.m; ++e) {
+      const uint64_t diff = ((x >> __ldg(el.ei + e)) ^ (x >> __ldg(el.ej + e))) & 1ull;
+      v = __dadd_rn(v, diff ? __ldg(el.w + e) : 0.0);
+    }
+    const double2 a = amps[y];
+    acc += (a.x * a.x + a.y * a.y) * v;
+  }
+  const double t = block_sum<kBlock>(acc, scratch);
+  if (threadIdx.x == 0) partials[blockIdx.x] = t;
+}
+
+cudaError_t launch_cost_weighted(double2* amps, uint64_t n, uint64_t xbase, const int* ei,
+                                 const int* ej, const double* w, int m, double gamma,
+                                 cudaStream_t s) {
+  EdgeList el{ei, ej, w, m};
+  cost_weighted_kernel<<<grid_for(n, 1), kBlock, 0, s>>>(amps, n, xbase, el, 0.5 * gamma);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expectation_weighted(const double2* amps, uint64_t n, uint64_t xbase,
+                                        const int* ei, const int* ej, const double* w, int m,
+                                        double* partials, int grid, cudaStream_t s) {
+  EdgeList el{ei, ej, w, m};
+  expectation_weighted_kernel<<<grid, kBlock, 0, s>>>(amps, n, xbase, el, partials);
+  return cudaGetLastError();
+}
+
 // ---- norm^2 and max |a - b| (state.py:50-51, :152-156) ---------------------
 __global__ void norm_sq_kernel(const double2* __restrict__ amps, uint64_t n,
                                double* __restrict__ partials) {

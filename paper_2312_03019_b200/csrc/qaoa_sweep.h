@@ -61,6 +61,12 @@ cudaError_t launch_pack_chunks(const double2* amps, int n_local, int g, const in
                                double2* dst, cudaStream_t s);
 cudaError_t launch_unpack_chunks(double2* amps, int n_local, int g, const int* local_bits,
                                  const double2* src, cudaStream_t s);
+cudaError_t launch_cost_weighted(double2* amps, uint64_t n, uint64_t xbase, const int* ei,
+                                 const int* ej, const double* w, int m, double gamma,
+                                 cudaStream_t s);
+cudaError_t launch_expectation_weighted(const double2* amps, uint64_t n, uint64_t xbase,
+                                        const int* ei, const int* ej, const double* w, int m,
+                                        double* partials, int grid, cudaStream_t s);
 int reduce_grid();
 
 }  // namespace qb

@@ -101,6 +101,18 @@ class Engine:
         if self.graph_key != key:
             self.set_graph(g, x_hi, key=key)
 
+    def ensure_weights(self, g) -> None:
+        """Weighted edge list on the device (qaoa_set_weights), in Graph.edges order."""
+        key = ("w", g.n, tuple(g.edges))
+        if getattr(self, "_wkey", None) == key:
+            return
+        ei = np.ascontiguousarray(np.array([e[0] for e in g.edges], dtype=np.int32))
+        ej = np.ascontiguousarray(np.array([e[1] for e in g.edges], dtype=np.int32))
+        w = np.ascontiguousarray(np.array([e[2] for e in g.edges], dtype=np.float64))
+        self.call("qaoa_set_weights", len(g.edges), ei.ctypes.data_as(_lib._ip),
+                  ej.ctypes.data_as(_lib._ip), _lib.dptr(w))
+        self._wkey = key
+
     def write(self, amps: np.ndarray, offset: int = 0) -> None:
         a = np.ascontiguousarray(amps, dtype=np.complex128)
         self.call("qaoa_write_amplitudes", offset, a.size, _lib.dptr(a.view(np.float64)))

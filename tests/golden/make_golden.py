@@ -94,6 +94,27 @@ def main() -> None:
             "expectation": expectation(g, s),
         })
 
+    # --- weighted graphs: the "compressed" backend (cost.py:147-159) -----------
+    meta["weighted"] = []
+    wcases = [(f"w3r{n}", random_regular_graph(n, 3, weighted=True, seed=n), params_from_seed(3, n))
+              for n in (6, 8, 10, 12, 14)]
+    rngw = np.random.default_rng(2)
+    for k in range(8):
+        n = int(rngw.integers(2, 13))
+        edges = [(i, j, float(rngw.uniform(0.1, 1.0))) for i in range(n) for j in range(i + 1, n)
+                 if rngw.random() < 0.4] or [(0, 1, 0.5)]
+        p = int(rngw.integers(1, 5))
+        pr = QaoaParams(gamma=tuple(rngw.uniform(0.0, 2 * math.pi, p)),
+                        beta=tuple(rngw.uniform(0.0, math.pi, p)))
+        wcases.append((f"wacc{k}", Graph.from_edges(n, edges), pr))
+    for name, g, pr in wcases:
+        s = simulate(g, pr, "compressed")
+        arrays[f"wamps_{name}"] = s.amps
+        meta["weighted"].append({
+            "name": name, "n": g.n, "edges": [[i, j, w] for i, j, w in g.edges],
+            "gamma": list(pr.gamma), "beta": list(pr.beta), "expectation": expectation(g, s),
+        })
+
     # --- single cost layer / mixer layer on a random state (n = 10) ------------
     g = random_regular_graph(10, 3, seed=4)
     r = np.random.default_rng(5)

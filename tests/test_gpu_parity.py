@@ -217,3 +217,52 @@ def test_config_c3_exact_vs_fast_n30():
     assert ef == pytest.approx(ee, rel=EXP_RTOL)
     assert 0.0 <= ef <= g.tot_edge
     assert f.norm() == pytest.approx(1.0, abs=1e-12)
+
+
+def test_weighted_compressed_golden(golden):
+    """Weighted graphs through the compressed backend (cost.py:147-159) vs the
+    reference's own runs: totals are bit-identical, only the device sincos
+    differs from glibc's by <= 2 ulp."""
+    meta, arrays = golden
+    for case in meta["weighted"]:
+        g = Q.Graph.from_edges(case["n"], [tuple(e) for e in case["edges"]])
+        assert not g.is_unweighted
+        pr = Q.QaoaParams(tuple(case["gamma"]), tuple(case["beta"]))
+        for backend in ("compressed", "baseline"):
+            s = Q.simulate(g, pr, backend)
+            assert np.max(np.abs(s.amps - arrays["wamps_" + case["name"]])) <= AMP_TOL, case["name"]
+            assert Q.expectation(g, s) == pytest.approx(case["expectation"], rel=EXP_RTOL, abs=1e-12)
+        with pytest.raises(ValueError, match="unweighted"):
+            Q.simulate(g, pr, "bitwise")
+
+
+def test_weighted_expectation_bounds():
+    g = Q.random_regular_graph(8, 3, weighted=True, seed=2)
+    for seed in range(10):
+        rng = np.random.default_rng(seed)
+        amps = rng.normal(size=256) + 1j * rng.normal(size=256)
+        amps /= np.linalg.norm(amps)
+        val = Q.expectation(g, Q.StateVector(8, amps))
+        assert 0 <= val <= g.total_weight + 1e-12
+        ref = float(np.sum(np.abs(amps) ** 2 * np.array([Q.cut_value(g, b) for b in range(256)])))
+        assert val == pytest.approx(ref, rel=1e-12)
+
+
+def test_weighted_larger_against_unweighted_limit():
+    """All-ones weights through the weighted kernel equal the integer path."""
+    g = Q.random_regular_graph(20, 3, seed=5)
+    gw = Q.Graph.from_edges(20, [(i, j, 1.0 + 1e-300) for i, j, _ in g.edges])
+    pr = Q.QaoaParams((0.7, 2.1), (0.4, 1.9))
+    a = Q.simulate(g, pr, "bitwise", exact=True)
+    # identical weights but flagged weighted: force the compressed weighted kernels
+    s = Q.init_uniform(20)
+    plan = Q.CompressedCostPlan(g)
+    from paper_2312_03019_b200 import cost as C
+    eng = s.engine()
+    eng.ensure_graph(g)
+    eng.ensure_weights(g)
+    for gm, bt in zip(pr.gamma, pr.beta):
+        eng.call("qaoa_apply_cost_weighted", gm)
+        Q.apply_mixer_layer(s, bt)
+    assert np.max(np.abs(s.amps - a.amps)) <= AMP_TOL
+    assert eng.scalar("qaoa_expectation_weighted") == pytest.approx(Q.expectation(g, a), rel=1e-12)
