@@ -146,6 +146,18 @@ QAOA_API int qaoa_set_weights(qaoa_ctx* ctx, int m, const int* ei, const int* ej
 QAOA_API int qaoa_apply_cost_weighted(qaoa_ctx* ctx, double gamma);
 QAOA_API int qaoa_expectation_weighted(qaoa_ctx* ctx, double* out);
 
+/* Sampling support (sample, circuit.py:124-133).  qaoa_block_norms: sum of
+ * |amp|^2 over each block of 2^block_bits consecutive TRUE indices (block_bits
+ * <= 12) into out[2^(n - block_bits)].  qaoa_sample_blocks: for each group g
+ * (one hit block group_block[g] with cumulative base group_base[g] = sum of
+ * the preceding blocks), the targets t in [group_off[g], group_off[g+1]) get
+ * out_idx = first true index x in the block with base + cumsum(|a|^2)(x) > t
+ * (numpy's searchsorted(cdf, u, 'right') on the unnormalised cdf). */
+QAOA_API int qaoa_block_norms(qaoa_ctx* ctx, int block_bits, double* out);
+QAOA_API int qaoa_sample_blocks(qaoa_ctx* ctx, int block_bits, int64_t n_groups,
+                                const int64_t* group_block, const double* group_base,
+                                const int64_t* group_off, const double* targets, int64_t* out_idx);
+
 /* Partial sum of |amp|^2 over the local shard (StateVector.norm, state.py:50-51). */
 QAOA_API int qaoa_norm_sq(qaoa_ctx* ctx, double* out);
 

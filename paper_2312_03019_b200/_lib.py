@@ -67,6 +67,8 @@ SIGNATURES = {
     "qaoa_apply_cost_weighted": (_c_int, [_vp, _c_dbl]),
     "qaoa_expectation_weighted": (_c_int, [_vp, _dp]),
     "qaoa_norm_sq": (_c_int, [_vp, _dp]),
+    "qaoa_block_norms": (_c_int, [_vp, _c_int, _dp]),
+    "qaoa_sample_blocks": (_c_int, [_vp, _c_int, ctypes.c_int64, _i64p, _dp, _i64p, _dp, _i64p]),
     "qaoa_max_abs_diff": (_c_int, [_vp, _vp, _dp]),
     "qaoa_build_cut_table": (_c_int, [_vp]),
     "qaoa_read_cut_table": (_c_int, [_vp, _u64, _u64, _i64p]),

@@ -196,6 +196,42 @@ def expectation(g: Graph, s: StateVector) -> float:
     return eng.scalar("qaoa_expectation")
 
 
+def sample(s: StateVector, shots: int, seed: int = 0) -> np.ndarray:
+    """Draw basis indices with probability |amp|^2 (circuit.py:124-133) without
+    moving the state off the device: the same uniforms as numpy's
+    ``default_rng(seed).choice(size, shots, p=probs/total)`` (cdf search,
+    side='right'), the cdf evaluated on the GPU per 4096-amplitude block."""
+    if shots < 1:
+        raise ValueError("shots must be at least 1")
+    import ctypes
+
+    eng = s.engine()
+    bb = min(s.n, 12)
+    norms = np.empty(1 << (s.n - bb), dtype=np.float64)
+    eng.call("qaoa_block_norms", bb, _lib.dptr(norms))
+    prefix = np.cumsum(norms)
+    total = float(prefix[-1])
+    if abs(total - 1.0) > 1e-6:
+        raise ValueError(f"state is not normalized (norm^2 = {total!r})")
+    u = np.random.default_rng(seed).random(shots)
+    targets = u * total
+    blk = np.minimum(np.searchsorted(prefix, targets, side="right"), prefix.size - 1)
+    order = np.argsort(blk, kind="stable")
+    sb = blk[order]
+    groups, starts = np.unique(sb, return_index=True)
+    offs = np.append(starts, shots).astype(np.int64)
+    base = np.where(groups > 0, prefix[np.maximum(groups - 1, 0)], 0.0).astype(np.float64)
+    t_sorted = np.ascontiguousarray(targets[order])
+    out_sorted = np.empty(shots, dtype=np.int64)
+    gblk = np.ascontiguousarray(groups.astype(np.int64))
+    eng.call("qaoa_sample_blocks", bb, ctypes.c_int64(groups.size),
+             gblk.ctypes.data_as(_lib._i64p), _lib.dptr(base), offs.ctypes.data_as(_lib._i64p),
+             _lib.dptr(t_sorted), out_sorted.ctypes.data_as(_lib._i64p))
+    out = np.empty(shots, dtype=np.int64)
+    out[order] = out_sorted
+    return out
+
+
 def gate_counts(n: int, g: Graph, p: int) -> tuple[int, int, int]:
     """(H, RZZ, RX) counts without launch control (circuit.py:136-138)."""
     return n, p * g.tot_edge, p * n

@@ -813,6 +813,54 @@ int qaoa_expectation_weighted(qaoa_ctx* c, double* out) {
   return reduce_to_host(c, grid, 0, out);
 }
 
+int qaoa_block_norms(qaoa_ctx* c, int block_bits, double* out) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (block_bits < 0 || block_bits > 12 || block_bits > c->n || !out)
+    return fail(QAOA_E_INVALID, "bad block size");
+  const uint64_t nb = 1ull << (c->n - block_bits);
+  double* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, nb * sizeof(double)));
+  cudaError_t e = launch_block_norms(c->amps, block_bits, nb, c->g.cmask & local_mask(c), d, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, nb * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "qaoa_block_norms");
+  return QAOA_OK;
+}
+
+int qaoa_sample_blocks(qaoa_ctx* c, int block_bits, int64_t n_groups, const int64_t* group_block,
+                       const double* group_base, const int64_t* group_off, const double* targets,
+                       int64_t* out_idx) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (block_bits < 0 || block_bits > 12 || block_bits > c->n || n_groups < 0)
+    return fail(QAOA_E_INVALID, "bad sampling arguments");
+  if (n_groups == 0) return QAOA_OK;
+  const int64_t shots = group_off[n_groups];
+  void* mem = nullptr;
+  const size_t bytes = n_groups * (sizeof(int64_t) + sizeof(double)) + (n_groups + 1) * sizeof(int64_t) +
+                       shots * (sizeof(double) + sizeof(int64_t));
+  CUDA_TRY(cudaMalloc(&mem, bytes));
+  char* p = (char*)mem;
+  int64_t* d_gb = (int64_t*)p; p += n_groups * sizeof(int64_t);
+  double* d_base = (double*)p; p += n_groups * sizeof(double);
+  int64_t* d_off = (int64_t*)p; p += (n_groups + 1) * sizeof(int64_t);
+  double* d_t = (double*)p; p += shots * sizeof(double);
+  int64_t* d_out = (int64_t*)p;
+  cudaError_t e = cudaMemcpyAsync(d_gb, group_block, n_groups * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_base, group_base, n_groups * sizeof(double), cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_off, group_off, (n_groups + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_t, targets, shots * sizeof(double), cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = launch_sample_blocks(c->amps, block_bits, c->g.cmask & local_mask(c), n_groups, d_gb,
+                                                 d_base, d_off, d_t, d_out, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out_idx, d_out, shots * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(mem);
+  if (e != cudaSuccess) return cuda_fail(e, "qaoa_sample_blocks");
+  return QAOA_OK;
+}
+
 int qaoa_expectation(qaoa_ctx* c, double* out) {
   int rc = check_ctx(c);
   if (rc) return rc;

@@ -218,6 +218,87 @@ cudaError_t launch_expectation_weighted(const double2* amps, uint64_t n, uint64_
   return cudaGetLastError();
 }
 
+// ---- sampling (circuit.py:124-133): numpy's Generator.choice(p=|a|^2) is
+// cdf = cumsum(p) / cdf[-1]; idx = searchsorted(cdf, uniform, 'right').  The
+// device computes |a|^2 block sums in true index order (kernel 1); the host
+// prefix-sums the blocks and assigns each target to a block; kernel 2 scans
+// each hit block once in shared memory and binary-searches its targets.
+constexpr int kSampleBlockMax = 4096;
+
+__global__ void block_norms_kernel(const double2* __restrict__ amps, int block_bits,
+                                   uint64_t lmask, double* __restrict__ out) {
+  __shared__ double scratch[kBlock / 32];
+  const uint64_t base = (uint64_t)blockIdx.x << block_bits;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < (1 << block_bits); i += kBlock) {
+    const double2 a = amps[(base + i) ^ lmask];
+    acc += a.x * a.x + a.y * a.y;
+  }
+  const double t = block_sum<kBlock>(acc, scratch);
+  if (threadIdx.x == 0) out[blockIdx.x] = t;
+}
+
+__global__ void sample_blocks_kernel(const double2* __restrict__ amps, int block_bits,
+                                     uint64_t lmask, const int64_t* __restrict__ gblock,
+                                     const double* __restrict__ gbase,
+                                     const int64_t* __restrict__ goff,
+                                     const double* __restrict__ targets,
+                                     int64_t* __restrict__ out) {
+  __shared__ double cdf[kSampleBlockMax];
+  __shared__ double wsum[kBlock / 32];
+  const int64_t blk = gblock[blockIdx.x];
+  const uint64_t base = (uint64_t)blk << block_bits;
+  const int len = 1 << block_bits;
+  const int per = (len + kBlock - 1) / kBlock;  // contiguous run per thread
+  const int lo = threadIdx.x * per;
+  double run = 0.0;
+  for (int i = lo; i < lo + per && i < len; ++i) {
+    const double2 a = amps[(base + i) ^ lmask];
+    run += a.x * a.x + a.y * a.y;
+    cdf[i] = run;
+  }
+  // exclusive prefix of the per-thread run totals (warp scan, then warps)
+  double x = run;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  double off = gbase[blockIdx.x];
+  for (int w = 0; w < warp; ++w) off += wsum[w];
+  off += x - run;
+  for (int i = lo; i < lo + per && i < len; ++i) cdf[i] += off;
+  __syncthreads();
+  for (int64_t s = goff[blockIdx.x] + threadIdx.x; s < goff[blockIdx.x + 1]; s += kBlock) {
+    const double t = targets[s];
+    int a = 0, b = len;  // first i with cdf[i] > t
+    while (a < b) {
+      const int m = (a + b) >> 1;
+      if (cdf[m] > t) b = m;
+      else a = m + 1;
+    }
+    out[s] = (int64_t)base + (a < len ? a : len - 1);
+  }
+}
+
+cudaError_t launch_block_norms(const double2* amps, int block_bits, uint64_t n_blocks,
+                               uint64_t lmask, double* out, cudaStream_t s) {
+  block_norms_kernel<<<(unsigned)n_blocks, kBlock, 0, s>>>(amps, block_bits, lmask, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample_blocks(const double2* amps, int block_bits, uint64_t lmask,
+                                 int64_t n_groups, const int64_t* gblock, const double* gbase,
+                                 const int64_t* goff, const double* targets, int64_t* out,
+                                 cudaStream_t s) {
+  sample_blocks_kernel<<<(unsigned)n_groups, kBlock, 0, s>>>(amps, block_bits, lmask, gblock, gbase,
+                                                              goff, targets, out);
+  return cudaGetLastError();
+}
+
 // ---- norm^2 and max |a - b| (state.py:50-51, :152-156) ---------------------
 __global__ void norm_sq_kernel(const double2* __restrict__ amps, uint64_t n,
                                double* __restrict__ partials) {

@@ -136,3 +136,12 @@ def test_params_from_seed_matches_reference(golden):
         p = int(key[1:].split("_")[0])
         q = Q.params_from_seed(p, 0)
         assert list(q.gamma) == pr["gamma"] and list(q.beta) == pr["beta"]
+
+
+def test_linear_ramp_and_wrap():
+    from paper_2312_03019_b200.optimize import wrap_angles
+
+    pr = Q.linear_ramp_params(4)
+    assert pr.gamma[0] == pytest.approx(0.125 * math.pi / 2) and pr.beta[-1] == pytest.approx(0.125 * math.pi / 2)
+    w = wrap_angles(np.array([7.0, -1.0, 4.0, -0.5]), 2)
+    assert 0 <= w.gamma[0] < 2 * math.pi and 0 <= w.beta[1] < math.pi
