@@ -10,7 +10,7 @@ the device.  The 16 GiB state is far larger than L2 (126 MB), so no flush is
 needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--n 30] [--p 10] [--exact]
+                    [--qubits 30] [--levels 10] [--exact] [--graph u3r|er]
 
 N > 1 (one process per GPU via torch.distributed.run, NCCL): the same N=30
 state is sharded over the G ranks by its top log2(G) qubits (strong scaling,
@@ -54,14 +54,17 @@ def dist_env():
     return rank, world, local
 
 
-def init_dist(world: int, local: int):
+def init_dist(world: int, local: int, backend: str = "nccl"):
     if world <= 1:
         return None
     import torch
     import torch.distributed as dist
 
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:  # test mode: several ranks may share one GPU; exchanges stage through host memory
+        dist.init_process_group("gloo")
     return dist
 
 
@@ -219,7 +222,9 @@ def run_sharded(args, rank: int, world: int, local: int):
 
     if world & (world - 1):
         raise SystemExit("sharded mode needs a power-of-two GPU count")
-    dist = init_dist(world, local)
+    if args.share_device:
+        local = 0
+    dist = init_dist(world, local, args.dist_backend)
     torch.cuda.set_device(local)
     n, p = args.n, args.p
     gbits = world.bit_length() - 1
@@ -231,7 +236,8 @@ def run_sharded(args, rank: int, world: int, local: int):
 
     def step():
         simulate_sharded(g, params, [shard], exch, gbits)
-        part = torch.tensor([shard.expectation()], dtype=torch.float64, device=f"cuda:{local}")
+        dev = "cpu" if args.dist_backend == "gloo" else f"cuda:{local}"
+        part = torch.tensor([shard.expectation()], dtype=torch.float64, device=dev)
         allp = [torch.zeros_like(part) for _ in range(world)]
         tdist.all_gather(allp, part)
         return float(sum(t.item() for t in allp))  # rank order: deterministic
@@ -248,7 +254,7 @@ def run_sharded(args, rank: int, world: int, local: int):
         stop.record()
         torch.cuda.synchronize(local)
     dev_ms = start.elapsed_time(stop)
-    t = torch.tensor([dev_ms], device=f"cuda:{local}")
+    t = torch.tensor([dev_ms], device="cpu" if args.dist_backend == "gloo" else f"cuda:{local}")
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     dev_ms = float(t.item())
     layers = p * args.steps / (dev_ms * 1e-3)
@@ -266,6 +272,7 @@ def run_sharded(args, rank: int, world: int, local: int):
                        f"(top {gbits} qubits), NCCL P2P exchange",
                        "l2": "no flush: shards >> L2"},
             "amp_updates_per_s": layers * per_level, "expectation": val,
+            "test_mode": bool(args.share_device or args.dist_backend != "nccl"),
             "nvlink": {"bytes_per_level_per_rank_per_direction": xbytes,
                        "peak_GBps_per_direction": 770.0},
             "roofline": {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s",
@@ -441,15 +448,20 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=30)
+    ap.add_argument("--qubits", dest="n", type=int, default=30)
     ap.add_argument("--graph", choices=["u3r", "er"], default="u3r",
                     help="u3r = random 3-regular seed 0 (configs 0-2, 4); er = G(n, 0.5) seed 0 "
                          "(configs[3], the dense N=33 cut-table stress case)")
-    ap.add_argument("--p", type=int, default=10)
+    ap.add_argument("--levels", dest="p", type=int, default=10)
     ap.add_argument("--exact", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cut-table", action="store_true", help="also time the K1 cut-table builder")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo = test mode (exchanges staged through host memory)")
+    ap.add_argument("--share-device", action="store_true",
+                    help="test mode: every rank uses cuda:0 (correctness of the sharded path "
+                         "on a one-GPU box; not a performance number)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: one full state per rank (weak scaling) instead of sharding")
     args = ap.parse_args()

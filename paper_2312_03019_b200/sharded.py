@@ -219,27 +219,35 @@ class DistExchanger:
         import torch.distributed as dist
 
         G, r = self.world, self.rank
-        t = torch.view_as_real(self.shard.tensor())  # [2^n, 2] float64 (NCCL has no c128)
-        chunk = t.shape[0] // G
+        dev = torch.view_as_real(self.shard.tensor())  # [2^n, 2] float64 (NCCL has no c128)
+        # gloo moves host tensors only: stage device shards through host memory
+        host_staged = dev.is_cuda and dist.get_backend(self.group) == "gloo"
+        chunk = dev.shape[0] // G
         piece = min(self.piece, chunk)
         peers = [d for d in range(G) if d != r]
-        if self.staging is None or self.staging.shape[0] < piece * len(peers):
-            self.staging = torch.empty((piece * len(peers), 2), dtype=t.dtype, device=t.device)
+        sdev = torch.device("cpu") if host_staged else dev.device
+        if self.staging is None or self.staging.shape[0] < piece * len(peers) or \
+                self.staging.device != sdev:
+            self.staging = torch.empty((piece * len(peers), 2), dtype=dev.dtype, device=sdev)
+            self.sendbuf = torch.empty_like(self.staging) if host_staged else None
         self.shard.synchronize()
         for off in range(0, chunk, piece):
             ln = min(piece, chunk - off)
             ops = []
             for k, d in enumerate(peers):
-                ops.append(dist.P2POp(dist.isend, t[d * chunk + off: d * chunk + off + ln], d,
-                                      group=self.group))
+                src = dev[d * chunk + off: d * chunk + off + ln]
+                if host_staged:
+                    self.sendbuf[k * piece: k * piece + ln].copy_(src)
+                    src = self.sendbuf[k * piece: k * piece + ln]
+                ops.append(dist.P2POp(dist.isend, src, d, group=self.group))
                 ops.append(dist.P2POp(dist.irecv, self.staging[k * piece: k * piece + ln], d,
                                       group=self.group))
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
             for k, d in enumerate(peers):
-                t[d * chunk + off: d * chunk + off + ln].copy_(self.staging[k * piece: k * piece + ln])
-        if t.is_cuda:
-            torch.cuda.synchronize(t.device)
+                dev[d * chunk + off: d * chunk + off + ln].copy_(self.staging[k * piece: k * piece + ln])
+        if dev.is_cuda:
+            torch.cuda.synchronize(dev.device)
 
 
 # --------------------------------------------------------------------------

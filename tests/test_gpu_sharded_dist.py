@@ -1,0 +1,32 @@
+"""The sharded bench path end to end under torch.distributed.run on a one-GPU
+box: 2 and 4 ranks share cuda:0, exchanges over gloo staged through host
+memory (the NCCL path is the same code with device tensors).  <C> must equal
+the unsharded engine's."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+import paper_2312_03019_b200 as Q
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_torchrun_sharded_bench(world):
+    n, p = 22, 3
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world),
+           os.path.join(ROOT, "bench.py"), "--gpus", str(world), "--steps", "2", "--warmup", "3",
+           "--qubits", str(n), "--levels", str(p), "--dist-backend", "gloo", "--share-device"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    g = Q.random_regular_graph(n, 3, seed=0)
+    e = Q.expectation(g, Q.simulate(g, Q.params_from_seed(p, 0), "bitwise", max_qubits=n))
+    assert line["expectation"] == pytest.approx(e, rel=1e-10)
+    assert line["n_gpus"] == world and line["scaling"] == "strong" and line["test_mode"]
