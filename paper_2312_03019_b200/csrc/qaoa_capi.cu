@@ -677,6 +677,7 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
   const int64_t ntiles = 1ll << (n - 12);
   const int grid = (int)ntiles;  // one tile per CTA (see sweep_kernel)
   if (want_expect && (rc = ensure_partials(c, grid))) return rc;
+  int n_partials = grid;
 
   if (p == 0) {
     if (!from_state) {
@@ -745,7 +746,7 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
   if (!from_state) c->g.cmask = 0;
   if (flips) c->g.cmask ^= local_mask(c);
   if (want_expect) {
-    if ((rc = reduce_to_host(c, grid, 0, &c->expect_value))) return rc;
+    if ((rc = reduce_to_host(c, n_partials, 0, &c->expect_value))) return rc;
     ++c->last_launches;
     c->expect_valid = true;
   }

@@ -1,5 +1,6 @@
 // qaoa_sweep.h -- host-visible description of one fused sweep launch.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -20,6 +21,7 @@ enum SweepFlags : uint32_t {
 };
 
 struct SweepArgs {
+  CUtensorMap map;       // 5-D view of the state, one box = half a tile (TMA loads / prefetch)
   double2* amps;
   const double2* table;  // even phase-table entries (E+1) of the pre-stage cost step
   const double2* table2; // even phase-table entries (E+1) of the mid cost step
@@ -33,9 +35,20 @@ struct SweepArgs {
   double2 scale;
   int table_len;
   uint32_t flags;
+  int pf_dist;           // > 0: L2-prefetch tile (this tile + pf_dist) before loading this one
+  int pf_tensor;         // prefetch through `map` (2 TMA prefetches) instead of per-run bulk prefetches
 };
+// 5-D tensor map of the state for tile geometry (C, q) (qaoa_sweep_tma.cu).
+bool make_tile_map(CUtensorMap* map, void* amps, int n, int C, int q);
 
 size_t sweep_smem_bytes(int table_len);
+// Fast-schedule sweeps run on the persistent TMA-fed kernel (qaoa_sweep_tma.cu)
+// unless QAOA_SWEEP_IMPL=v4; sweep_grid() = CTAs launched = partials written.
+int sweep_impl(const SweepArgs& a);  // 0 one tile per CTA, 1 TMA-fed, 2 TMA in + out
+bool sweep_uses_tma(const SweepArgs& a);
+void set_sweep_impl(int v);  // force 0 / 1 / 2, or 3 = per-sweep policy (default); tooling / A-B tests
+int sweep_grid(const SweepArgs& a);
+cudaError_t launch_sweep_tma(const SweepArgs& a, cudaStream_t stream);
 cudaError_t launch_sweep(const SweepArgs& args, int grid, cudaStream_t stream);
 int sweep_max_grid(int table_len);
 

@@ -1,0 +1,308 @@
+// qaoa_tile.cuh -- device building blocks of the fused sweep kernels: the
+// 4096-amplitude tile geometry, the three register mappings and their
+// shared-memory exchanges, the per-tile cut-count basis (C(x) recomputed from
+// the row masks, bit-exact), the cost phase, the RX register butterflies and
+// the <C> accumulation.  Shared by qaoa_sweep.cu (one tile per CTA) and
+// qaoa_sweep_tma.cu (persistent, TMA-fed).
+#pragma once
+#include "qaoa_common.cuh"
+#include "qaoa_sweep.h"
+
+namespace qb {
+
+constexpr int kTileBits = 12;
+constexpr int kTile = 1 << kTileBits;
+constexpr int kThreads = 256;
+constexpr int kRegs = 16;
+// Shared-memory slot of tile index t: one 16-byte pad after every 16 slots, so
+// register r of every mapping sits at a compile-time offset from a per-thread
+// base (M2: +272 r, M0: +r, M1: +17 r) and every 8-lane phase of a 128-bit
+// access hits 8 distinct 16-byte bank groups.
+constexpr int kSlots = kTile + kTile / 16;
+__host__ __device__ constexpr int slot(int t) { return t + (t >> 4); }
+
+// Tile index of register r of thread tid in mapping M.  M3 / M4 are M2 / M1
+// after lane bit 3 and register bit 0 traded places (transpose_lane3): register
+// bit 0 then holds tile bit 3 and lane bit 3 holds tile bit 8 (M3) / 4 (M4).
+template <int M>
+__host__ __device__ constexpr int tile_index(int tid, int r) {
+  return M == 2 ? (tid | (r << 8))
+       : M == 0 ? ((tid << 4) | r)
+       : M == 1 ? ((tid & 15) | ((tid >> 4) << 8) | (r << 4))
+       : M == 3 ? ((tid & 0xF7) | (((tid >> 3) & 1) << 8) | ((r & 1) << 3) | ((r >> 1) << 9))
+                : ((tid & 7) | (((tid >> 3) & 1) << 4) | ((tid >> 4) << 8) | ((r & 1) << 3) |
+                   ((r >> 1) << 5));
+}
+template <int M>
+__host__ __device__ constexpr int group_of() {
+  return M == 2 ? 2 : (M == 0 ? 0 : 1);
+}
+
+// Physical offset of tile index t for carried-bit count C and high range at q.
+template <int C>
+__device__ __forceinline__ uint64_t tile_off(int t, uint64_t Q /* = 1 << q */) {
+  if (C >= 12) return (uint64_t)t;
+  return (uint64_t)(t & ((1 << C) - 1)) + (uint64_t)(t >> C) * Q;
+}
+template <int C>
+__device__ __forceinline__ int tile_pos(int k, int q) {  // physical bit of tile bit k
+  return (C >= 12 || k < C) ? k : q + (k - C);
+}
+
+// slot(thread part | register part) = slot(thread part) + slot(register part)
+// for every mapping (their low four bits never carry), so register offsets are
+// compile-time constants.
+template <int M>
+__device__ __forceinline__ void smem_store(double2* buf, int sb, const double2 (&v)[kRegs]) {
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) buf[sb + slot(tile_index<M>(0, r))] = v[r];
+}
+template <int M>
+__device__ __forceinline__ void smem_load(const double2* buf, int sb, double2 (&v)[kRegs]) {
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) v[r] = buf[sb + slot(tile_index<M>(0, r))];
+}
+
+struct ThreadSlots {
+  int s[5];
+};
+
+// Re-map registers from mapping A to mapping B through shared memory.  In a
+// later exchange every thread writes (in mapping B) exactly the slots it read
+// here, so one barrier per exchange suffices; the tile loop adds one barrier
+// before the first write of the next tile.
+template <int A, int B>
+__device__ __forceinline__ void exchange(double2* buf, const ThreadSlots& ts, double2 (&v)[kRegs]) {
+  smem_store<A>(buf, ts.s[A], v);
+  __syncthreads();
+  smem_load<B>(buf, ts.s[B], v);
+}
+
+// Same, for a 256-thread group of a larger CTA: named barrier `bar_id`.
+template <int A, int B>
+__device__ __forceinline__ void exchange_bar(double2* buf, const ThreadSlots& ts, double2 (&v)[kRegs],
+                                             int bar_id) {
+  smem_store<A>(buf, ts.s[A], v);
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(kThreads) : "memory");
+  smem_load<B>(buf, ts.s[B], v);
+}
+
+// Trade lane bit 3 for register bit 0 inside each warp: the lane with lane bit
+// 3 = 0 gives away its odd registers and receives the partner's even ones.  Half
+// the data crosses lanes (one shuffle per moved word, vs two-way for a lane
+// butterfly); afterwards tile bit 3 is a register bit (mappings M3 / M4).
+__device__ __forceinline__ void transpose_lane3(double2 (&v)[kRegs]) {
+  // The next exchange stores in the transposed mapping, i.e. to slots the
+  // partner lane read in the last exchange: order those reads first (the data
+  // dependency through the shuffles already does; this makes it explicit for
+  // the memory model and for racecheck).
+  __syncwarp();
+  const bool hi = (threadIdx.x & 8) != 0;
+#pragma unroll
+  for (int r = 0; r < kRegs; r += 2) {
+    const double2 snd = hi ? v[r] : v[r + 1];
+    double2 rcv;
+    rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, 8);
+    rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, 8);
+    if (hi) v[r] = rcv;
+    else v[r + 1] = rcv;
+  }
+}
+
+// Compile-time description of which tile bits a sweep mixes: bits C..11 (C<12)
+// or all 12 (C == 12).
+template <int C>
+struct Act {
+  static constexpr unsigned tile = C >= 12 ? 0xFFFu : ((0xFFFu >> C) << C);
+  static constexpr unsigned g0 = tile & 15u;
+  static constexpr unsigned g1 = (tile >> 4) & 15u;
+  static constexpr unsigned g2 = (tile >> 8) & 15u;
+  // a lone active bit 3 in group 0 is handled by lane shuffles (lane bit 3 in M2 and M1)
+  static constexpr bool g0_shfl = (g0 == 8u);
+  static constexpr bool g0_xchg = g0 != 0 && !g0_shfl;
+};
+
+// Physical index of element 0 of tile `tile`: tile bits cleared, the non-tile
+// bits [C, q) and [q + 12 - C, n) filled from the tile number (low part first).
+template <int C>
+__device__ __forceinline__ uint64_t tile_base(uint64_t tile, int q) {
+  const int low_bits = C >= 12 ? 0 : q - C;
+  return C >= 12 ? (tile << 12)
+                 : (((tile & ((1ull << low_bits) - 1ull)) << C) | ((tile >> low_bits) << (q + 12 - C)));
+}
+
+// L2 prefetch of a whole tile (its 2^(12-C) contiguous runs), spread over the
+// CTA's threads: the bulk-prefetch engine pulls the runs into L2 while the SM
+// works, so the tile's later loads hit L2 instead of HBM.
+template <int C, int THREADS>
+__device__ __forceinline__ void prefetch_tile_l2(const double2* amps, uint64_t base, uint64_t Q,
+                                                 int tid) {
+  constexpr int runs = C >= 12 ? 1 : (1 << (12 - C));
+  constexpr uint32_t run_bytes = C >= 12 ? 65536u : (16u << C);
+  for (int i = tid; i < runs; i += THREADS) {
+    const double2* p = amps + base + (C >= 12 ? 0ull : (uint64_t)i * Q);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(run_bytes) : "memory");
+  }
+}
+
+// TMA coordinates of half `h` of tile `tile` (dims as built by make_tile_map).
+template <int C>
+__device__ __forceinline__ void half_coords(const SweepArgs& a, uint64_t tile, int h, int (&c)[5]) {
+  c[0] = 0;
+  if (C >= 12) {
+    c[1] = 0; c[2] = h; c[3] = (int)tile; c[4] = 0;
+  } else {
+    const int low_bits = a.q - C;
+    const int low = (int)(tile & ((1ull << low_bits) - 1ull));
+    const int high = (int)(tile >> low_bits);
+    if (C == 3) {
+      c[1] = low; c[2] = 0; c[3] = h; c[4] = high;
+    } else {
+      c[1] = 0; c[2] = low; c[3] = h << (11 - C); c[4] = high;
+    }
+  }
+}
+struct TileCtx {
+  uint64_t base;           // physical index of tile element 0 (tile bits zero), without x_hi
+  uint64_t tb0, tb1, tb2;  // thread base offsets per mapping
+};
+
+// Per-tile cut-count basis, computed once per CTA by warp 0 (lane-parallel over
+// nodes).  h = true index of tile element 0 with all tile bits cleared
+// (x_hi ^ cmask ^ base, see GraphDev::cmask); K = C(h); per tile node k,
+// d[k] = deg(k) - 2 popc(adj[k] & h) (change of C when node k alone is set);
+// adjl[k] = tile-local neighbour mask (12 bits); tmask = cmask's tile bits (the
+// true tile bits of tile index t are t ^ tmask).
+struct CutBasis {
+  int K;
+  int tmask;
+  int d[12];
+  int adjl[12];
+};
+
+template <bool WIDE, int C>
+__device__ __forceinline__ void cut_basis(const SweepArgs& a, uint64_t base, int q, CutBasis* cb) {
+  const uint64_t tile_phys = (C >= 12) ? 0xFFFull
+                                       : (((1ull << C) - 1ull) | (((1ull << (12 - C)) - 1ull) << q));
+  const uint64_t h = (a.g.x_hi ^ a.g.cmask ^ base) & ~tile_phys;
+  const int lane = threadIdx.x & 31;
+  int part = 0;
+  for (int i = lane; i < a.g.n_nodes; i += 32) {
+    const uint64_t b = 0ull - ((h >> i) & 1ull);
+    part += __popcll(a.g.rm[i] & (b ^ h));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  const uint64_t cm = a.g.cmask;
+  const int tm = (int)((C >= 12) ? (cm & 0xFFFull)
+                                 : ((cm & ((1ull << C) - 1ull)) |
+                                    (((cm >> q) & ((1ull << (12 - C)) - 1ull)) << C)));
+  if (lane < 12) {
+    const int p = tile_pos<C>(lane, q);
+    const uint64_t m = a.g.adj[p];
+    cb->d[lane] = __popcll(m) - 2 * __popcll(m & h);
+    const uint32_t lo = (uint32_t)(m & ((C >= 12) ? 0xFFFull : ((1ull << C) - 1ull)));
+    const uint32_t hi = (C >= 12) ? 0u : (uint32_t)((m >> q) & ((1ull << (12 - C)) - 1ull)) << C;
+    cb->adjl[lane] = (int)(lo | hi);
+  }
+  if (lane == 0) {
+    cb->K = part;
+    cb->tmask = tm;
+  }
+}
+
+// C(x) for the 16 registers of mapping M.  With T = true tile bits of the
+// thread's register-0 element: C(h | T) = K + sum_{k in T} (d[k] - popc(adjl[k] & T));
+// flipping register node j changes C by s_j (d[j] - 2 popc(adjl[j] & T)) with
+// s_j = -1 if bit j of T is set, and each edge between two flipped nodes j, k
+// adds -2 s_j s_k.  Exact integer arithmetic.
+template <int M>
+__device__ __forceinline__ void cut16(const CutBasis* cb, int (&c)[16], int tid) {
+  const int T = tile_index<M>(tid, 0) ^ cb->tmask;
+  constexpr int g = group_of<M>();
+  int c0 = cb->K;
+#pragma unroll
+  for (int k = 0; k < 12; ++k)
+    if ((T >> k) & 1) c0 += cb->d[k] - __popc(cb->adjl[k] & T);
+  int d[4], al[4], sg[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    al[j] = cb->adjl[4 * g + j];
+    sg[j] = ((T >> (4 * g + j)) & 1) ? -1 : 1;
+    d[j] = sg[j] * (cb->d[4 * g + j] - 2 * __popc(al[j] & T));
+  }
+  const int a01 = 2 * sg[0] * sg[1] * ((al[0] >> (4 * g + 1)) & 1);
+  const int a02 = 2 * sg[0] * sg[2] * ((al[0] >> (4 * g + 2)) & 1);
+  const int a03 = 2 * sg[0] * sg[3] * ((al[0] >> (4 * g + 3)) & 1);
+  const int a12 = 2 * sg[1] * sg[2] * ((al[1] >> (4 * g + 2)) & 1);
+  const int a13 = 2 * sg[1] * sg[3] * ((al[1] >> (4 * g + 3)) & 1);
+  const int a23 = 2 * sg[2] * sg[3] * ((al[2] >> (4 * g + 3)) & 1);
+  c[0] = c0;
+  c[1] = c0 + d[0];
+  c[2] = c0 + d[1];
+  c[3] = c[1] + d[1] - a01;
+  c[4] = c0 + d[2];
+  c[5] = c[1] + d[2] - a02;
+  c[6] = c[2] + d[2] - a12;
+  c[7] = c[3] + d[2] - a02 - a12;
+  c[8] = c0 + d[3];
+  c[9] = c[1] + d[3] - a03;
+  c[10] = c[2] + d[3] - a13;
+  c[11] = c[3] + d[3] - a03 - a13;
+  c[12] = c[4] + d[3] - a23;
+  c[13] = c[5] + d[3] - a03 - a23;
+  c[14] = c[6] + d[3] - a13 - a23;
+  c[15] = c[7] + d[3] - a03 - a13 - a23;
+}
+
+// amp *= table_even[E - C(x)] (table_even[k] = phase_table[2k]; reference
+// cost.py:168-172 indexes table[(E - 2C) + E]).
+template <int M>
+__device__ __forceinline__ void apply_cost(double2 (&v)[kRegs], const CutBasis* cb,
+                                           const double2* __restrict__ tab, int e,
+                                           int tid = threadIdx.x) {
+  int c[16];
+  cut16<M>(cb, c, tid);
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], __ldg(tab + (e - c[r])));
+}
+
+template <int M>
+__device__ __forceinline__ double expect_acc(const double2 (&v)[kRegs], const CutBasis* cb,
+                                             int tid = threadIdx.x) {
+  int c[16];
+  cut16<M>(cb, c, tid);
+  double acc = 0.0;
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) acc += (v[r].x * v[r].x + v[r].y * v[r].y) * (double)c[r];
+  return acc;
+}
+
+// RX(stage) on register bits MASK: exact (reference rounding) or the factored
+// fast form mine - i t other (form-2 levels run as form 1 with t = -k plus a
+// global bit complement tracked on the host; see qaoa_capi.cu).
+template <unsigned MASK, bool EXACT>
+__device__ __forceinline__ void rx_regs2(double2 (&v)[kRegs], double c_or_t, double s) {
+#pragma unroll
+  for (int K = 0; K < 4; ++K) {
+    if (!((MASK >> K) & 1)) continue;
+#pragma unroll
+    for (int r = 0; r < kRegs; ++r) {
+      if (r & (1 << K)) continue;
+      if (EXACT) rx_exact(v[r], v[r | (1 << K)], c_or_t, s);
+      else rx_form1(v[r], v[r | (1 << K)], c_or_t);
+    }
+  }
+}
+
+template <int C, int M>
+__device__ __forceinline__ void store_tile(double2* __restrict__ amps, const TileCtx& tc,
+                                           uint64_t Q, const double2 (&v)[kRegs], uint32_t flags) {
+  if (flags & kNoStore) return;
+  const uint64_t tb = M == 2 ? tc.tb2 : tc.tb1;
+  double2* dst = amps + tc.base + tb;
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) __stcs(dst + tile_off<C>(tile_index<M>(0, r), Q), v[r]);
+}
+
+}  // namespace qb
