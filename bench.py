@@ -94,7 +94,7 @@ class ClockSampler:
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,power.draw,enforced.power.limit,clocks.mem")
 
     def __init__(self, index: int):
         self.index = index
@@ -126,7 +126,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
+        sm, mx, reasons, pw, lim, mem = [], 0.0, set(), [], [], []
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         for ln in self.lines:
             parts = [x.strip() for x in ln.split(",")]
@@ -137,13 +137,25 @@ class ClockSampler:
                 mx = max(mx, float(parts[1]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[2:]):
+            for nm, v in zip(names, parts[2:6]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
+            for dst, i in ((pw, 6), (lim, 7), (mem, 8)):
+                try:
+                    dst.append(float(parts[i]))
+                except (IndexError, ValueError):
+                    pass
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+               "samples": len(sm)}
+        if pw:
+            out["power_w"] = statistics.median(pw)
+        if lim:
+            out["power_limit_w"] = statistics.median(lim)
+        if mem:
+            out["mem_mhz"] = statistics.median(mem)
+        return out
 
 
 def cpu_reference_rate(threads: int, levels: int = 1):
@@ -355,7 +367,10 @@ def run_ours(args, rank: int, world: int, local: int):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "peak_kind": peak_kind,
-                "kernel": "qb::sweep_kernel (fused cost+RX sweep)",
+                "kernel": "fused cost+RX sweeps (qb::sweep_kernel one tile per CTA + L2 prefetch; "
+                          "qb::sweep_tma_kernel persistent TMA-fed for the launch-control and "
+                          "top-set merged sweeps)",
+                "launch_ms_last_step": [round(x, 3) for x in launch_ms[-sweeps_per_step:]],
                 "algorithmic_bytes_per_launch": 32 * (1 << n),
                 "launches_per_step": sweeps_per_step,
                 "avg_launch_ms": step_sweep_ms / max(sweeps_per_step, 1),

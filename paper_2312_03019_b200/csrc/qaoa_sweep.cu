@@ -47,7 +47,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   __shared__ CutBasis cb;
   __shared__ double red_scratch[kThreads / 32];
   using A = Act<C>;
-  constexpr bool EX = FLOW == 0;
+  // skewed register layout for the fast C = 3 flows (select-free transposes)
+  const int sk = (FLOW != 0 && A::g0_shfl) ? lane_skew() : 0;
 
   const uint32_t flags = a.flags;
   const int tid = threadIdx.x;
@@ -90,9 +91,12 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         }
       }
     }
-    const double2* src = amps + tc.base + tc.tb2;
+    const int64_t d = sk ? (int64_t)tile_off<C>(tile_index<2>(0, 1), Q) : 0;
+    const double2* se = amps + tc.base + tc.tb2 + d;
+    const double2* so = amps + tc.base + tc.tb2 - d;
 #pragma unroll
-    for (int r = 0; r < kRegs; ++r) v[r] = __ldcs(src + tile_off<C>(tile_index<2>(0, r), Q));
+    for (int r = 0; r < kRegs; ++r)
+      v[r] = __ldcs(((r & 1) ? so : se) + tile_off<C>(tile_index<2>(0, r), Q));
   }
   const bool need_cut = flags & (kPreCost | kMidCost | kExpect);
   if (need_cut) {
@@ -159,32 +163,32 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     }
   } else {
     // ---- fast, high set: G2 (+ tile bit 3), G1 [, cost, G1 (+ tile bit 3), G2]
-    if (flags & kPreCost) apply_cost<2>(v, &cb, a.table, e);
+    if (flags & kPreCost) apply_cost<2>(v, &cb, a.table, e, tid, sk);
     rx_regs2<A::g2, false>(v, r1a, 0.0);
     if (A::g0_shfl) {  // C = 3: tile bit 3 traded into register bit 0 (M2 -> M3)
-      transpose_lane3(v);
+      transpose_lane3_sk(v);
       rx_regs2<1u, false>(v, r1a, 0.0);
-      exchange<3, 1>(buf, ts, v);
+      exchange<3, 1>(buf, ts, v, sk);
       rx_regs2<A::g1, false>(v, r1a, 0.0);
       if (FLOW == 2) {
-        apply_cost<1>(v, &cb, a.table2, e);
+        apply_cost<1>(v, &cb, a.table2, e, tid, sk);
         rx_regs2<A::g1, false>(v, r2a, 0.0);
-        transpose_lane3(v);  // M1 -> M4
+        transpose_lane3_sk(v);  // M1 -> M4
         rx_regs2<1u, false>(v, r2a, 0.0);
-        exchange<4, 2>(buf, ts, v);
+        exchange<4, 2>(buf, ts, v, sk);
         rx_regs2<A::g2, false>(v, r2a, 0.0);
       }
     } else if (A::g1) {
-      exchange<2, 1>(buf, ts, v);
+      exchange<2, 1>(buf, ts, v, sk);
       rx_regs2<A::g1, false>(v, r1a, 0.0);
       if (FLOW == 2) {
-        apply_cost<1>(v, &cb, a.table2, e);
+        apply_cost<1>(v, &cb, a.table2, e, tid, sk);
         rx_regs2<A::g1, false>(v, r2a, 0.0);
-        exchange<1, 2>(buf, ts, v);
+        exchange<1, 2>(buf, ts, v, sk);
         rx_regs2<A::g2, false>(v, r2a, 0.0);
       }
     } else if (FLOW == 2) {
-      apply_cost<2>(v, &cb, a.table2, e);
+      apply_cost<2>(v, &cb, a.table2, e, tid, sk);
       rx_regs2<A::g2, false>(v, r2a, 0.0);
     }
     constexpr int last = (A::g1 && FLOW == 1) ? 1 : 2;
@@ -192,8 +196,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
 #pragma unroll
       for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
     }
-    if (flags & kExpect) acc = expect_acc<last>(v, &cb);
-    store_tile<C, last>(amps, tc, Q, v, flags);
+    if (flags & kExpect) acc = expect_acc<last>(v, &cb, tid, sk);
+    store_tile<C, last>(amps, tc, Q, v, flags, sk);
   }
   if (flags & kExpect) {
     const double t = block_sum<kThreads>(acc, red_scratch);

@@ -112,17 +112,19 @@ __device__ __forceinline__ void issue_half(const TmaSweepArgs& a, void* dst, uin
 template <int C, int M, bool TS>
 __device__ __forceinline__ void finish_tile(const TmaSweepArgs& ta, const TileCtx& tc, uint64_t Q,
                                             const double2 (&v)[kRegs], double2* buf, int tid,
-                                            int bar_id, uint64_t tile) {
+                                            int bar_id, uint64_t tile, int sk) {
   const uint32_t flags = ta.s.flags;
   if (!TS) {
-    store_tile<C, M>(ta.s.amps, tc, Q, v, flags);
+    store_tile<C, M>(ta.s.amps, tc, Q, v, flags, sk);
     return;
   }
   if (flags & kNoStore) return;
   group_bar(bar_id);  // every thread has read its last exchange slots
-  double2* dst = buf + tile_index<M>(tid, 0);
+  constexpr int D = tile_index<M>(0, 1);
+  double2* de = buf + tile_index<M>(tid, 0) + sk * D;
+  double2* dodd = buf + tile_index<M>(tid, 0) - sk * D;
 #pragma unroll
-  for (int r = 0; r < kRegs; ++r) dst[tile_index<M>(0, r)] = v[r];
+  for (int r = 0; r < kRegs; ++r) ((r & 1) ? dodd : de)[tile_index<M>(0, r)] = v[r];
   fence_async_smem();  // generic-proxy writes -> visible to the TMA (async proxy)
   group_bar(bar_id);
   if (tid == 0) {
@@ -151,6 +153,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
   __shared__ CutBasis cbs[kGroups][2];
   using A = Act<C>;
   static_assert(FLOW == 1 || FLOW == 2, "fast flows only");
+  const int sk = A::g0_shfl ? lane_skew() : 0;  // skewed register layout (qaoa_tile.cuh)
   const SweepArgs& a = ta.s;
   const uint32_t flags = a.flags;
   const int bar_id = 1 + grp;
@@ -232,9 +235,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if (h == 1) mbar_wait(&full[2 + grp], j & 1);
-        const double2* src = land + h * (kTile / 2) + tid;
+        const double2* se = land + h * (kTile / 2) + tid + (sk << 8);
+        const double2* so = land + h * (kTile / 2) + tid - (sk << 8);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) v[8 * h + r] = src[r << 8];
+        for (int r = 0; r < 8; ++r) v[8 * h + r] = ((r & 1) ? so : se)[r << 8];
         // order these generic-proxy reads before the TMA refill of the slot
         // (without it the refill was observed to overtake them)
         fence_async_smem();
@@ -277,43 +281,43 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
           for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
         }
         if (flags & kExpect) acc += expect_acc<2>(v, cb, tid);
-        finish_tile<C, 2, TS>(ta, tc, Q, v, buf, tid, bar_id, tile);
+        finish_tile<C, 2, TS>(ta, tc, Q, v, buf, tid, bar_id, tile, 0);
       } else {
         if (flags & kScale) {
 #pragma unroll
           for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
         }
         if (flags & kExpect) acc += expect_acc<1>(v, cb, tid);
-        finish_tile<C, 1, TS>(ta, tc, Q, v, buf, tid, bar_id, tile);
+        finish_tile<C, 1, TS>(ta, tc, Q, v, buf, tid, bar_id, tile, 0);
       }
     } else {
       // ---- high set: G2 (+ tile bit 3), G1 [, cost, G1 (+ tile bit 3), G2]
-      if (flags & kPreCost) apply_cost<2>(v, cb, a.table, e, tid);
+      if (flags & kPreCost) apply_cost<2>(v, cb, a.table, e, tid, sk);
       rx_regs2<A::g2, false>(v, r1a, 0.0);
       if (A::g0_shfl) {
-        transpose_lane3(v);
+        transpose_lane3_sk(v);
         rx_regs2<1u, false>(v, r1a, 0.0);
-        exchange_bar<3, 1>(buf, ts, v, bar_id);
+        exchange_bar<3, 1>(buf, ts, v, bar_id, sk);
         rx_regs2<A::g1, false>(v, r1a, 0.0);
         if (FLOW == 2) {
-          apply_cost<1>(v, cb, a.table2, e, tid);
+          apply_cost<1>(v, cb, a.table2, e, tid, sk);
           rx_regs2<A::g1, false>(v, r2a, 0.0);
-          transpose_lane3(v);
+          transpose_lane3_sk(v);
           rx_regs2<1u, false>(v, r2a, 0.0);
-          exchange_bar<4, 2>(buf, ts, v, bar_id);
+          exchange_bar<4, 2>(buf, ts, v, bar_id, sk);
           rx_regs2<A::g2, false>(v, r2a, 0.0);
         }
       } else if (A::g1) {
-        exchange_bar<2, 1>(buf, ts, v, bar_id);
+        exchange_bar<2, 1>(buf, ts, v, bar_id, sk);
         rx_regs2<A::g1, false>(v, r1a, 0.0);
         if (FLOW == 2) {
-          apply_cost<1>(v, cb, a.table2, e, tid);
+          apply_cost<1>(v, cb, a.table2, e, tid, sk);
           rx_regs2<A::g1, false>(v, r2a, 0.0);
-          exchange_bar<1, 2>(buf, ts, v, bar_id);
+          exchange_bar<1, 2>(buf, ts, v, bar_id, sk);
           rx_regs2<A::g2, false>(v, r2a, 0.0);
         }
       } else if (FLOW == 2) {
-        apply_cost<2>(v, cb, a.table2, e, tid);
+        apply_cost<2>(v, cb, a.table2, e, tid, sk);
         rx_regs2<A::g2, false>(v, r2a, 0.0);
       }
       constexpr int last_m = (A::g1 && FLOW == 1) ? 1 : 2;
@@ -321,8 +325,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
 #pragma unroll
         for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
       }
-      if (flags & kExpect) acc += expect_acc<last_m>(v, cb, tid);
-      finish_tile<C, last_m, TS>(ta, tc, Q, v, buf, tid, bar_id, tile);
+      if (flags & kExpect) acc += expect_acc<last_m>(v, cb, tid, sk);
+      finish_tile<C, last_m, TS>(ta, tc, Q, v, buf, tid, bar_id, tile, sk);
     }
     if (flags & kExpect) {
       // per-tile partial (fixed shuffle tree, warps in order): the sum over
@@ -487,8 +491,8 @@ void set_sweep_impl(int v) { g_impl = v; }
 // Which kernel runs a fast-schedule sweep (0: one tile per CTA, qaoa_sweep.cu;
 // 1: persistent TMA-fed, register stores; 2: persistent TMA-fed, TMA stores).
 // Measured on B200 at N=30 (tools/sweep_probe.cu, ms per sweep):
-//   launch-control (kGen) sweep      v4 4.59 | TMA in/out 4.19          -> 2
-//   merged sweep of the top set      v4 8.09 | TMA-fed 7.63             -> 1
+//   launch-control (kGen) sweep      v4 4.48 | TMA in/out 4.10          -> 2
+//   merged sweep of the top set      v4 7.85 | TMA-fed 7.96 | in/out 7.57 -> 2
 //   (tile spans > 256 MB: 512 DRAM pages per tile, L2 prefetch hurts)
 //   everything else                  v4 + L2 prefetch is fastest        -> 0
 int sweep_impl(const SweepArgs& a) {
@@ -497,7 +501,7 @@ int sweep_impl(const SweepArgs& a) {
   if (env != 3) return env;
   if (a.flags & kGen) return 2;
   const bool wide_span = a.carry < 12 && a.q + 12 - a.carry + 4 > 28;
-  if ((a.flags & kStage2) && wide_span) return 1;
+  if ((a.flags & kStage2) && wide_span) return 2;
   return 0;
 }
 

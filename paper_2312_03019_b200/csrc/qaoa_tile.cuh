@@ -52,15 +52,29 @@ __device__ __forceinline__ int tile_pos(int k, int q) {  // physical bit of tile
 // slot(thread part | register part) = slot(thread part) + slot(register part)
 // for every mapping (their low four bits never carry), so register offsets are
 // compile-time constants.
+//
+// Skewed layout (sk = 1, the C = 3 fast flows): in lanes with lane bit 3 set,
+// physical register p holds logical register p ^ 1.  The lane-bit-3 <->
+// register-bit-0 transpose then moves the odd physical registers of every lane
+// (no selects or predicated moves), the RX butterflies are symmetric in their
+// two operands, and the cut counts follow from a shifted thread base (cut16);
+// only the even / odd registers' memory bases differ by one register-bit-0
+// step.  sk = 0 is the plain layout.
 template <int M>
-__device__ __forceinline__ void smem_store(double2* buf, int sb, const double2 (&v)[kRegs]) {
+__device__ __forceinline__ void smem_store(double2* buf, int sb, const double2 (&v)[kRegs],
+                                           int sk = 0) {
+  constexpr int D = slot(tile_index<M>(0, 1));
+  const int se = sb + sk * D, so = sb - sk * D;
 #pragma unroll
-  for (int r = 0; r < kRegs; ++r) buf[sb + slot(tile_index<M>(0, r))] = v[r];
+  for (int r = 0; r < kRegs; ++r) buf[((r & 1) ? so : se) + slot(tile_index<M>(0, r))] = v[r];
 }
 template <int M>
-__device__ __forceinline__ void smem_load(const double2* buf, int sb, double2 (&v)[kRegs]) {
+__device__ __forceinline__ void smem_load(const double2* buf, int sb, double2 (&v)[kRegs],
+                                          int sk = 0) {
+  constexpr int D = slot(tile_index<M>(0, 1));
+  const int se = sb + sk * D, so = sb - sk * D;
 #pragma unroll
-  for (int r = 0; r < kRegs; ++r) v[r] = buf[sb + slot(tile_index<M>(0, r))];
+  for (int r = 0; r < kRegs; ++r) v[r] = buf[((r & 1) ? so : se) + slot(tile_index<M>(0, r))];
 }
 
 struct ThreadSlots {
@@ -72,19 +86,20 @@ struct ThreadSlots {
 // here, so one barrier per exchange suffices; the tile loop adds one barrier
 // before the first write of the next tile.
 template <int A, int B>
-__device__ __forceinline__ void exchange(double2* buf, const ThreadSlots& ts, double2 (&v)[kRegs]) {
-  smem_store<A>(buf, ts.s[A], v);
+__device__ __forceinline__ void exchange(double2* buf, const ThreadSlots& ts, double2 (&v)[kRegs],
+                                         int sk = 0) {
+  smem_store<A>(buf, ts.s[A], v, sk);
   __syncthreads();
-  smem_load<B>(buf, ts.s[B], v);
+  smem_load<B>(buf, ts.s[B], v, sk);
 }
 
 // Same, for a 256-thread group of a larger CTA: named barrier `bar_id`.
 template <int A, int B>
 __device__ __forceinline__ void exchange_bar(double2* buf, const ThreadSlots& ts, double2 (&v)[kRegs],
-                                             int bar_id) {
-  smem_store<A>(buf, ts.s[A], v);
+                                             int bar_id, int sk = 0) {
+  smem_store<A>(buf, ts.s[A], v, sk);
   asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(kThreads) : "memory");
-  smem_load<B>(buf, ts.s[B], v);
+  smem_load<B>(buf, ts.s[B], v, sk);
 }
 
 // Trade lane bit 3 for register bit 0 inside each warp: the lane with lane bit
@@ -108,6 +123,20 @@ __device__ __forceinline__ void transpose_lane3(double2 (&v)[kRegs]) {
     else v[r + 1] = rcv;
   }
 }
+
+// The same transpose in the skewed layout: every lane sends and receives its
+// odd physical registers (4 shuffles per moved amplitude, nothing else).
+__device__ __forceinline__ void transpose_lane3_sk(double2 (&v)[kRegs]) {
+  __syncwarp();  // see transpose_lane3
+#pragma unroll
+  for (int r = 1; r < kRegs; r += 2) {
+    v[r].x = __shfl_xor_sync(0xffffffffu, v[r].x, 8);
+    v[r].y = __shfl_xor_sync(0xffffffffu, v[r].y, 8);
+  }
+}
+
+// Lane bit 3 of the calling thread: the skew of the C = 3 fast flows.
+__device__ __forceinline__ int lane_skew() { return (threadIdx.x >> 3) & 1; }
 
 // Compile-time description of which tile bits a sweep mixes: bits C..11 (C<12)
 // or all 12 (C == 12).
@@ -217,8 +246,9 @@ __device__ __forceinline__ void cut_basis(const SweepArgs& a, uint64_t base, int
 // s_j = -1 if bit j of T is set, and each edge between two flipped nodes j, k
 // adds -2 s_j s_k.  Exact integer arithmetic.
 template <int M>
-__device__ __forceinline__ void cut16(const CutBasis* cb, int (&c)[16], int tid) {
-  const int T = tile_index<M>(tid, 0) ^ cb->tmask;
+__device__ __forceinline__ void cut16(const CutBasis* cb, int (&c)[16], int tid, int sk = 0) {
+  // skewed layout: physical register 0 holds logical register sk
+  const int T = tile_index<M>(tid, 0) ^ cb->tmask ^ (sk ? tile_index<M>(0, 1) : 0);
   constexpr int g = group_of<M>();
   int c0 = cb->K;
 #pragma unroll
@@ -260,18 +290,18 @@ __device__ __forceinline__ void cut16(const CutBasis* cb, int (&c)[16], int tid)
 template <int M>
 __device__ __forceinline__ void apply_cost(double2 (&v)[kRegs], const CutBasis* cb,
                                            const double2* __restrict__ tab, int e,
-                                           int tid = threadIdx.x) {
+                                           int tid = threadIdx.x, int sk = 0) {
   int c[16];
-  cut16<M>(cb, c, tid);
+  cut16<M>(cb, c, tid, sk);
 #pragma unroll
   for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], __ldg(tab + (e - c[r])));
 }
 
 template <int M>
 __device__ __forceinline__ double expect_acc(const double2 (&v)[kRegs], const CutBasis* cb,
-                                             int tid = threadIdx.x) {
+                                             int tid = threadIdx.x, int sk = 0) {
   int c[16];
-  cut16<M>(cb, c, tid);
+  cut16<M>(cb, c, tid, sk);
   double acc = 0.0;
 #pragma unroll
   for (int r = 0; r < kRegs; ++r) acc += (v[r].x * v[r].x + v[r].y * v[r].y) * (double)c[r];
@@ -297,12 +327,16 @@ __device__ __forceinline__ void rx_regs2(double2 (&v)[kRegs], double c_or_t, dou
 
 template <int C, int M>
 __device__ __forceinline__ void store_tile(double2* __restrict__ amps, const TileCtx& tc,
-                                           uint64_t Q, const double2 (&v)[kRegs], uint32_t flags) {
+                                           uint64_t Q, const double2 (&v)[kRegs], uint32_t flags,
+                                           int sk = 0) {
   if (flags & kNoStore) return;
   const uint64_t tb = M == 2 ? tc.tb2 : tc.tb1;
-  double2* dst = amps + tc.base + tb;
+  const int64_t d = sk ? (int64_t)tile_off<C>(tile_index<M>(0, 1), Q) : 0;
+  double2* de = amps + tc.base + tb + d;
+  double2* dodd = amps + tc.base + tb - d;
 #pragma unroll
-  for (int r = 0; r < kRegs; ++r) __stcs(dst + tile_off<C>(tile_index<M>(0, r), Q), v[r]);
+  for (int r = 0; r < kRegs; ++r)
+    __stcs(((r & 1) ? dodd : de) + tile_off<C>(tile_index<M>(0, r), Q), v[r]);
 }
 
 }  // namespace qb
