@@ -230,7 +230,8 @@ def run_sharded(args, rank: int, world: int, local: int):
     import torch.distributed as tdist
 
     import paper_2312_03019_b200 as Q
-    from paper_2312_03019_b200.sharded import CudaShard, DistExchanger, simulate_sharded
+    from paper_2312_03019_b200.sharded import (CudaShard, DistExchanger, IpcExchanger,
+                                               simulate_sharded, simulate_sharded_fused)
 
     if world & (world - 1):
         raise SystemExit("sharded mode needs a power-of-two GPU count")
@@ -242,12 +243,16 @@ def run_sharded(args, rank: int, world: int, local: int):
     gbits = world.bit_length() - 1
     g = make_graph(Q, args)
     params = Q.params_from_seed(p, 0)
+    fused = args.exchange == "ipc"
     shard = CudaShard(n - gbits, rank, device=local, exact=args.exact,
-                      stream=torch.cuda.current_stream(local).cuda_stream)
-    exch = DistExchanger(shard, rank, world)
+                      stream=None if fused else torch.cuda.current_stream(local).cuda_stream)
+    exch = IpcExchanger(shard, rank, world) if fused else DistExchanger(shard, rank, world)
 
     def step():
-        simulate_sharded(g, params, [shard], exch, gbits)
+        if fused:
+            simulate_sharded_fused(g, params, [shard], exch, gbits, exact=args.exact, expect=True)
+        else:
+            simulate_sharded(g, params, [shard], exch, gbits)
         dev = "cpu" if args.dist_backend == "gloo" else f"cuda:{local}"
         part = torch.tensor([shard.expectation()], dtype=torch.float64, device=dev)
         allp = [torch.zeros_like(part) for _ in range(world)]
@@ -477,6 +482,9 @@ def main():
     ap.add_argument("--share-device", action="store_true",
                     help="test mode: every rank uses cuda:0 (correctness of the sharded path "
                          "on a one-GPU box; not a performance number)")
+    ap.add_argument("--exchange", choices=["ipc", "nccl"], default="ipc",
+                    help="sharded runs: fused exchange kernel over CUDA-IPC peer pointers "
+                         "(default) or the NCCL P2P staging path")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: one full state per rank (weak scaling) instead of sharding")
     args = ap.parse_args()

@@ -42,6 +42,7 @@ extern "C" {
 #define QAOA_RUN_FROM_STATE 0x2     /* start from the resident state, not |+>^n         */
 #define QAOA_RUN_EXPECTATION 0x4    /* fuse <C> into the last sweep (qaoa_expectation)  */
 #define QAOA_RUN_TIMING 0x8         /* record per-launch CUDA-event times               */
+#define QAOA_RUN_SHARDED 0x10       /* qaoa_run_begin: exchange points after S_0 of every level */
 
 typedef struct qaoa_ctx qaoa_ctx;
 
@@ -188,6 +189,42 @@ QAOA_API int qaoa_synchronize(qaoa_ctx* ctx);
  * chunks.  The engine exposes pack/unpack so the host can drive NCCL or P2P. */
 QAOA_API int qaoa_pack_chunks(qaoa_ctx* ctx, int g, const int* local_bits, void* dst_device);
 QAOA_API int qaoa_unpack_chunks(qaoa_ctx* ctx, int g, const int* local_bits, const void* src_device);
+
+/* ---- planned runs in segments (sharded states) -----------------------------
+ * qaoa_run_layers = qaoa_run_begin + every qaoa_run_segment + qaoa_run_end.
+ * With QAOA_RUN_SHARDED the plan stops after the low qubit set S_0 (local bits
+ * 0..11) of every level: segment k is followed by the exchange of
+ * qaoa_run_exchange_info(k) (all shards: host barrier, qaoa_exchange, barrier,
+ * qaoa_set_graph with the relabelled masks, qaoa_set_cmask), and level flips
+ * complement all n_nodes bits of the complement mask.  Requires n_local >= 12. */
+QAOA_API int qaoa_run_begin(qaoa_ctx* ctx, int p, const double* phase_tables, const double* c,
+                            const double* s, int flags, int* n_segments);
+QAOA_API int qaoa_run_segment(qaoa_ctx* ctx, int k);
+/* Exchange after segment k: the level whose RX the arriving qubits need, its
+ * RX stage (rx[0..2] = a, b, mode: 0 exact (c, s), 1 factored t) and its
+ * per-qubit scale factor (factor[0..1] = re, im; 1 in exact mode).  Returns
+ * QAOA_E_RANGE when no exchange follows segment k. */
+QAOA_API int qaoa_run_exchange_info(qaoa_ctx* ctx, int k, int* level, double* rx, double* factor);
+QAOA_API int qaoa_run_end(qaoa_ctx* ctx);
+
+/* ---- fused exchange + RX over shard pointers ------------------------------
+ * G = 2^g shards (g <= 4) of 2^n_local amplitudes; shards[r] is a device
+ * pointer to shard r valid on `device` (local buffer, CUDA-IPC mapped peer
+ * buffer, or another buffer on the same device for virtual shards).  Swaps
+ * global bit k with local bit p0 + k and applies RX (rx as above) to the
+ * arriving qubits, multiplying by factor^g; processes y in [y_lo, y_hi) of the
+ * 2^(n_local - g) column indices (split them across the ranks).  Stream-ordered
+ * on `stream` (NULL: legacy default stream); the caller synchronises the ranks
+ * before (all segments done) and after (all writes landed). */
+QAOA_API int qaoa_exchange(int device, void* stream, int g, void* const* shards, int n_local, int p0,
+                           uint64_t y_lo, uint64_t y_hi, const double* rx, const double* factor);
+
+/* ---- CUDA IPC (one process per GPU) ----------------------------------------
+ * 64-byte handle of the context's state buffer; open a peer's handle on
+ * `device` (peer access over NVLink) and close it again. */
+QAOA_API int qaoa_ipc_handle(qaoa_ctx* ctx, void* handle64);
+QAOA_API int qaoa_ipc_open(const void* handle64, int device, void** out_ptr);
+QAOA_API int qaoa_ipc_close(void* ptr);
 
 #ifdef __cplusplus
 }

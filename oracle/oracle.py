@@ -204,6 +204,51 @@ class OracleShard:
     def synchronize(self):
         pass
 
+    # segmented protocol of the fused sharded path (sharded.simulate_sharded_fused):
+    # segment k = cost_k + RX_k on every local qubit; the exchange after it
+    # applies RX_k (exact form) to the arriving qubits; the last segment is empty.
+    def run_begin(self, tables, cs, ss, flags):
+        self._run = (np.asarray(tables), np.asarray(cs), np.asarray(ss))
+        return len(cs) + 1
+
+    def run_segment(self, k):
+        tables, cs, ss = self._run
+        if k < len(cs):
+            self.run_level(tables[k], float(cs[k]), float(ss[k]), first=(k == 0))
+
+    def exchange_info(self, k):
+        tables, cs, ss = self._run
+        if k >= len(cs):
+            return None
+        return k, np.array([cs[k], ss[k], 0.0]), np.array([1.0, 0.0])
+
+    def run_end(self):
+        pass
+
+    def state_ptr(self):
+        return self
+
+
+def fused_exchange_numpy(arrays, g, p0, rx):
+    """CPU restatement of the fused exchange kernel (qaoa_exchange.cu) on G numpy
+    shards in place: element (shard r, local (y, h)) -> (shard h, local (y, r)),
+    then the exact RX (c = rx[0], s = rx[1], reference rounding, state.py:114-124)
+    on the arriving bits p0.. of every shard, bit by bit in increasing order."""
+    G = 1 << g
+    n = int(arrays[0].size).bit_length() - 1
+    lo = 1 << p0
+    mid = 1 << g
+    hi = 1 << (n - p0 - g)
+    views = [a.reshape(hi, mid, lo) for a in arrays]
+    old = [v.copy() for v in views]
+    for h in range(G):
+        for r in range(G):
+            views[h][:, r, :] = old[r][:, h, :]
+    c, s = float(rx[0]), float(rx[1])
+    for a in arrays:
+        for k in range(g):
+            lib().orc_apply_rx(n, p0 + k, c, s, _ptr(a, _f64p), 1)
+
 
 # ---------------------------------------------------------------------------
 # Input generators restated from the reference (needed on the GPU box, where

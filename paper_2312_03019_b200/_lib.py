@@ -30,6 +30,7 @@ RUN_EXACT = 0x1
 RUN_FROM_STATE = 0x2
 RUN_EXPECTATION = 0x4
 RUN_TIMING = 0x8
+RUN_SHARDED = 0x10
 
 _c_int = ctypes.c_int
 _c_dbl = ctypes.c_double
@@ -78,6 +79,15 @@ SIGNATURES = {
     "qaoa_synchronize": (_c_int, [_vp]),
     "qaoa_pack_chunks": (_c_int, [_vp, _c_int, _ip, _vp]),
     "qaoa_unpack_chunks": (_c_int, [_vp, _c_int, _ip, _vp]),
+    "qaoa_run_begin": (_c_int, [_vp, _c_int, _dp, _dp, _dp, _c_int, _ip]),
+    "qaoa_run_segment": (_c_int, [_vp, _c_int]),
+    "qaoa_run_exchange_info": (_c_int, [_vp, _c_int, _ip, _dp, _dp]),
+    "qaoa_run_end": (_c_int, [_vp]),
+    "qaoa_exchange": (_c_int, [_c_int, _vp, _c_int, ctypes.POINTER(_vp), _c_int, _c_int, _u64, _u64,
+                               _dp, _dp]),
+    "qaoa_ipc_handle": (_c_int, [_vp, _vp]),
+    "qaoa_ipc_open": (_c_int, [_vp, _c_int, ctypes.POINTER(_vp)]),
+    "qaoa_ipc_close": (_c_int, [_vp]),
 }
 
 _lib = None

@@ -63,6 +63,26 @@ struct SweepPlan {
   int stage1;    // level index or -1
   int mid_cost;  // level index or -1
   int stage2;    // level index or -1
+  int exchange;  // sharded runs: level whose global<->local exchange follows, or -1
+};
+
+// A planned run, executed in segments separated by the exchanges of a sharded
+// state (qaoa_run_begin / qaoa_run_segment / qaoa_run_end); qaoa_run_layers is
+// begin + every segment + end.
+struct RunState {
+  bool active = false;
+  bool exact = false, want_expect = false, timing = false, from_state = false, sharded = false;
+  int p = 0;
+  std::vector<SetDesc> sets;
+  std::vector<SweepPlan> plan;
+  std::vector<RxStage> stages;
+  std::vector<std::complex<double>> level_factor;  // per-qubit RX scale of each level (fast)
+  std::complex<double> final_scale{1.0, 0.0};
+  int flips = 0;
+  std::vector<int> seg_start;  // segment k = plan[seg_start[k], seg_start[k + 1])
+  size_t ev = 0;
+  int grid = 0;
+  bool expect_fused = false;
 };
 
 }  // namespace
@@ -102,6 +122,7 @@ struct qaoa_ctx {
   std::vector<float> times;
   int last_launches = 0;
   double last_bytes = 0.0;
+  RunState run;
 };
 
 namespace {
@@ -158,10 +179,13 @@ std::vector<SetDesc> make_sets(int n) {
   return sets;
 }
 
-std::vector<SweepPlan> make_plan(int n_sets, int p, bool exact) {
-  // flat op list: cost l, then mixer l over the sets in this level's order
+std::vector<SweepPlan> make_plan(int n_sets, int p, bool exact, bool sharded = false) {
+  // flat op list: cost l, then mixer l over the sets in this level's order;
+  // sharded: an exchange (kind 2) right after the low set S_0 of every level
+  // (the swapped local bits sit in S_0, so they have had RX_l when they leave
+  // and the arriving ones get RX_l inside the exchange kernel)
   struct Op {
-    int kind;  // 0 cost, 1 mixer
+    int kind;  // 0 cost, 1 mixer, 2 exchange
     int level;
     int set;
   };
@@ -180,12 +204,16 @@ std::vector<SweepPlan> make_plan(int n_sets, int p, bool exact) {
   for (int l = 0; l < p; ++l) {
     ops.push_back({0, l, -1});
     const bool fwd = exact || (l % 2 == 0);
-    for (int i = 0; i < n_sets; ++i) ops.push_back({1, l, fwd ? order[i] : order[n_sets - 1 - i]});
+    for (int i = 0; i < n_sets; ++i) {
+      const int set = fwd ? order[i] : order[n_sets - 1 - i];
+      ops.push_back({1, l, set});
+      if (sharded && set == 0) ops.push_back({2, l, -1});
+    }
   }
   std::vector<SweepPlan> plan;
   size_t i = 0;
   while (i < ops.size()) {
-    SweepPlan sp{-1, -1, -1, -1, -1};
+    SweepPlan sp{-1, -1, -1, -1, -1, -1};
     if (ops[i].kind == 0) {
       sp.pre_cost = ops[i].level;
       ++i;
@@ -199,6 +227,10 @@ std::vector<SweepPlan> make_plan(int n_sets, int p, bool exact) {
       sp.mid_cost = ops[i].level;
       sp.stage2 = ops[i + 1].level;
       i += 2;
+    }
+    if (i < ops.size() && ops[i].kind == 2) {
+      sp.exchange = ops[i].level;
+      ++i;
     }
     plan.push_back(sp);
   }
@@ -289,6 +321,188 @@ int create_common(int n, int device, void* stream, void* ext, qaoa_ctx** out) {
     return rc;
   }
   *out = c;
+  return QAOA_OK;
+}
+
+
+// ---- planned runs: begin / segment / end ----------------------------------
+// Tiled states (n_local >= 12).  sharded: exchange points after S_0 of every
+// level (make_plan), level flips complement all n_nodes bits (the host's
+// cmask covers the shard bits too), <C> is fused only when the run does not end
+// on an exchange.
+int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, const double* sn,
+              int flags, bool sharded) {
+  RunState& R = c->run;
+  R = RunState();
+  R.exact = flags & QAOA_RUN_EXACT;
+  R.from_state = flags & QAOA_RUN_FROM_STATE;
+  R.want_expect = flags & QAOA_RUN_EXPECTATION;
+  R.timing = flags & QAOA_RUN_TIMING;
+  R.sharded = sharded;
+  R.p = p;
+  const int n = c->n;
+  const int n_total = c->g.n_nodes;
+  const double u = sqrt(1.0 / (double)(1ull << n_total));
+  const uint64_t size = 1ull << n;
+  c->expect_valid = false;
+  c->last_launches = 0;
+  c->last_bytes = 0.0;
+  c->times.clear();
+  int rc;
+  if (!R.from_state) c->g.cmask = 0;
+
+  R.sets = make_sets(n);
+  R.plan = make_plan((int)R.sets.size(), p, R.exact, sharded);
+
+  // phase tables: the sweeps only index even entries (t = E - 2C), so upload
+  // table_even[k] = table[2k], k = 0..E.  exact = as given; fast = scaled by
+  // the previous level's factor.
+  const int tl = 2 * c->g.tot_edge + 1;
+  const int te = c->g.tot_edge + 1;
+  R.stages.assign(std::max(p, 1), RxStage{0.0, 0.0, 0});
+  R.level_factor.assign(std::max(p, 1), std::complex<double>(1.0, 0.0));
+  std::complex<double> prev_scale(1.0, 0.0);
+  if ((rc = ensure_tables(c, (size_t)te * std::max(p, 1)))) return rc;
+  for (int l = 0; l < p; ++l) {
+    const std::complex<double> f_scale = prev_scale;
+    const double* src = phase_tables + (size_t)2 * tl * l;
+    for (int k = 0; k < te; ++k) {
+      std::complex<double> v(src[4 * k], src[4 * k + 1]);
+      if (!R.exact) v *= f_scale;
+      c->h_tables[(size_t)l * te + k] = make_double2(v.real(), v.imag());
+    }
+    if (R.exact) {
+      R.stages[l] = RxStage{cs[l], sn[l], 0};
+    } else if (std::fabs(cs[l]) >= std::fabs(sn[l])) {
+      // RX = c [[1, -i t], [-i t, 1]], t = s / c
+      R.stages[l] = RxStage{sn[l] / cs[l], 0.0, 1};
+      R.level_factor[l] = std::complex<double>(cs[l], 0.0);
+      prev_scale = std::pow(R.level_factor[l], n);
+    } else {
+      // RX = (-i s) X [[1, i k], [i k, 1]], k = c / s: run form 1 with t = -k and
+      // complement every bit (X^n) by bookkeeping instead of data movement.
+      R.stages[l] = RxStage{-cs[l] / sn[l], 0.0, 1};
+      R.level_factor[l] = std::complex<double>(0.0, -sn[l]);
+      prev_scale = std::pow(R.level_factor[l], n);
+      R.flips ^= 1;
+    }
+  }
+  if (p > 0)
+    CUDA_TRY(cudaMemcpyAsync(c->d_tables, c->h_tables, sizeof(double2) * (size_t)te * p,
+                             cudaMemcpyHostToDevice, c->stream));
+  R.final_scale = R.exact ? std::complex<double>(1.0, 0.0) : prev_scale;
+
+  const int64_t ntiles = 1ll << (n - 12);
+  R.grid = (int)ntiles;  // partials: one per tile
+  if (R.want_expect && (rc = ensure_partials(c, R.grid))) return rc;
+
+  if (p == 0) {
+    if (!R.from_state) {
+      CUDA_TRY(launch_fill(c->amps, size, make_double2(u, 0.0), c->stream));
+      ++c->last_launches;
+      c->last_bytes += 16.0 * size;
+    }
+    if (R.want_expect) {
+      const int g2 = reduce_grid();
+      CUDA_TRY(launch_expectation(c->amps, n, c->g, c->partials, g2, c->stream));
+      ++c->last_launches;
+      if ((rc = reduce_to_host(c, g2, 0, &c->expect_value))) return rc;
+      c->expect_valid = true;
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return QAOA_OK;
+  }
+  R.seg_start.push_back(0);
+  for (size_t i = 0; i < R.plan.size(); ++i)
+    if (R.plan[i].exchange >= 0) R.seg_start.push_back((int)i + 1);
+  if (R.seg_start.back() != (int)R.plan.size()) R.seg_start.push_back((int)R.plan.size());
+  R.expect_fused = R.want_expect && R.plan.back().exchange < 0;
+  R.active = true;
+  if ((rc = record_event(c, R.timing, R.ev++))) return rc;
+  return QAOA_OK;
+}
+
+int run_segment(qaoa_ctx* c, int k) {
+  RunState& R = c->run;
+  if (!R.active) return fail(QAOA_E_STATE, "no planned run (qaoa_run_begin)");
+  if (k < 0 || k + 1 >= (int)R.seg_start.size()) return fail(QAOA_E_RANGE, "segment out of range");
+  const uint64_t size = 1ull << c->n;
+  const int te = c->g.tot_edge + 1;
+  const double u = sqrt(1.0 / (double)(1ull << c->g.n_nodes));
+  int rc;
+  for (int i = R.seg_start[k]; i < R.seg_start[k + 1]; ++i) {
+    const SweepPlan& sp = R.plan[i];
+    const SetDesc& st = R.sets[sp.set];
+    SweepArgs a;
+    memset(&a, 0, sizeof(a));
+    a.amps = c->amps;
+    a.g = c->g;
+    a.ntiles = 1ll << (c->n - 12);
+    a.partials = c->partials;
+    a.carry = st.carry;
+    a.q = st.q;
+    uint32_t fl = R.exact ? kExact : 0u;
+    if (i == 0 && !R.from_state) {
+      fl |= kGen;
+      a.gen = make_double2(u, 0.0);
+    }
+    a.table_len = te;
+    if (sp.pre_cost >= 0) {
+      fl |= kPreCost;
+      a.table = c->d_tables + (size_t)sp.pre_cost * te;
+    }
+    if (sp.mid_cost >= 0) {
+      fl |= kMidCost;
+      a.table2 = c->d_tables + (size_t)sp.mid_cost * te;
+    }
+    if (sp.stage1 >= 0) {
+      fl |= kStage1;
+      a.rx1 = R.stages[sp.stage1];
+    }
+    if (sp.stage2 >= 0) {
+      fl |= kStage2;
+      a.rx2 = R.stages[sp.stage2];
+    }
+    const bool last = i + 1 == (int)R.plan.size();
+    if (last && !R.exact) {
+      fl |= kScale;
+      a.scale = make_double2(R.final_scale.real(), R.final_scale.imag());
+    }
+    if (last && R.expect_fused) fl |= kExpect;
+    a.flags = fl;
+    CUDA_TRY(launch_sweep(a, R.grid, c->stream));
+    ++c->last_launches;
+    c->last_bytes += ((fl & kGen) ? 16.0 : 32.0) * (double)size;
+    if ((rc = record_event(c, R.timing, R.ev++))) return rc;
+  }
+  return QAOA_OK;
+}
+
+int run_end(qaoa_ctx* c) {
+  RunState& R = c->run;
+  if (!R.active) return fail(QAOA_E_STATE, "no planned run (qaoa_run_begin)");
+  R.active = false;
+  int rc;
+  if (R.flips) {
+    // sharded: complement all n_nodes bits (C(x) = C(~x) keeps the cost kernels
+    // exact with the run's initial mask); unsharded: all local bits = all bits
+    const uint64_t all = R.sharded ? (c->g.n_nodes >= 64 ? ~0ull : ((1ull << c->g.n_nodes) - 1ull))
+                                   : local_mask(c);
+    c->g.cmask ^= all;
+  }
+  if (R.expect_fused) {
+    if ((rc = reduce_to_host(c, R.grid, 0, &c->expect_value))) return rc;
+    ++c->last_launches;
+    c->expect_valid = true;
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (R.timing) {
+    for (size_t i = 0; i + 1 < R.ev; ++i) {
+      float ms = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&ms, c->events[i], c->events[i + 1]));
+      c->times.push_back(ms);
+    }
+  }
   return QAOA_OK;
 }
 
@@ -636,128 +850,108 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
   }
 
   // ---- tiled path --------------------------------------------------------
-  const std::vector<SetDesc> sets = make_sets(n);
-  std::vector<SweepPlan> plan = make_plan((int)sets.size(), p, exact);
+  if ((rc = run_begin(c, p, phase_tables, cs, sn, flags, false))) return rc;
+  if (p == 0) return QAOA_OK;  // handled (fill / expectation) inside run_begin
+  for (size_t k = 0; k + 1 < c->run.seg_start.size(); ++k)
+    if ((rc = run_segment(c, (int)k))) return rc;
+  return run_end(c);
+}
 
-  // phase tables: the sweeps only index even entries (t = E - 2C), so upload
-  // table_even[k] = table[2k], k = 0..E.  exact = as given; fast = scaled by
-  // the previous level's factor.
-  const int te = c->g.tot_edge + 1;
-  std::vector<RxStage> stages(std::max(p, 1));
-  std::complex<double> prev_scale(1.0, 0.0);
-  int flips = 0;
-  if ((rc = ensure_tables(c, (size_t)te * std::max(p, 1)))) return rc;
-  for (int l = 0; l < p; ++l) {
-    const std::complex<double> f_scale = prev_scale;
-    const double* src = phase_tables + (size_t)2 * tl * l;
-    for (int k = 0; k < te; ++k) {
-      std::complex<double> v(src[4 * k], src[4 * k + 1]);
-      if (!exact) v *= f_scale;
-      c->h_tables[(size_t)l * te + k] = make_double2(v.real(), v.imag());
-    }
-    if (exact) {
-      stages[l] = RxStage{cs[l], sn[l], 0};
-    } else if (std::fabs(cs[l]) >= std::fabs(sn[l])) {
-      // RX = c [[1, -i t], [-i t, 1]], t = s / c
-      stages[l] = RxStage{sn[l] / cs[l], 0.0, 1};
-      prev_scale = std::pow(std::complex<double>(cs[l], 0.0), n);
-    } else {
-      // RX = (-i s) X [[1, i k], [i k, 1]], k = c / s: run form 1 with t = -k and
-      // complement every bit (X^n) by bookkeeping instead of data movement.
-      stages[l] = RxStage{-cs[l] / sn[l], 0.0, 1};
-      prev_scale = std::pow(std::complex<double>(0.0, -sn[l]), n);
-      flips ^= 1;
-    }
-  }
-  if (p > 0)
-    CUDA_TRY(cudaMemcpyAsync(c->d_tables, c->h_tables, sizeof(double2) * (size_t)te * p,
-                             cudaMemcpyHostToDevice, c->stream));
-  const std::complex<double> final_scale = exact ? std::complex<double>(1.0, 0.0) : prev_scale;
+int qaoa_run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs,
+                   const double* sn, int flags, int* n_segments) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (!c->has_graph) return fail(QAOA_E_STATE, "no graph set");
+  if (p < 1) return fail(QAOA_E_INVALID, "planned runs need at least one level");
+  if (!phase_tables || !cs || !sn) return fail(QAOA_E_INVALID, "null angle arrays");
+  if (c->n < 12) return fail(QAOA_E_INVALID, "planned runs need at least 12 local qubits");
+  if ((rc = run_begin(c, p, phase_tables, cs, sn, flags, (flags & QAOA_RUN_SHARDED) != 0))) return rc;
+  if (n_segments) *n_segments = (int)c->run.seg_start.size() - 1;
+  return QAOA_OK;
+}
 
-  const int64_t ntiles = 1ll << (n - 12);
-  const int grid = (int)ntiles;  // one tile per CTA (see sweep_kernel)
-  if (want_expect && (rc = ensure_partials(c, grid))) return rc;
-  int n_partials = grid;
+int qaoa_run_segment(qaoa_ctx* c, int k) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  return run_segment(c, k);
+}
 
-  if (p == 0) {
-    if (!from_state) {
-      c->g.cmask = 0;
-      CUDA_TRY(launch_fill(c->amps, size, make_double2(u, 0.0), c->stream));
-      ++c->last_launches;
-      c->last_bytes += 16.0 * size;
-    }
-    if (want_expect) {
-      const int g2 = reduce_grid();
-      CUDA_TRY(launch_expectation(c->amps, n, c->g, c->partials, g2, c->stream));
-      ++c->last_launches;
-      if ((rc = reduce_to_host(c, g2, 0, &c->expect_value))) return rc;
-      c->expect_valid = true;
-    }
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    return QAOA_OK;
+int qaoa_run_exchange_info(qaoa_ctx* c, int k, int* level, double* rx, double* factor) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  const RunState& R = c->run;
+  if (!R.active) return fail(QAOA_E_STATE, "no planned run (qaoa_run_begin)");
+  if (k < 0 || k + 1 >= (int)R.seg_start.size()) return fail(QAOA_E_RANGE, "segment out of range");
+  const int l = R.plan[R.seg_start[k + 1] - 1].exchange;
+  if (l < 0) return fail(QAOA_E_RANGE, "no exchange after this segment");
+  if (level) *level = l;
+  if (rx) {
+    rx[0] = R.stages[l].a;
+    rx[1] = R.stages[l].b;
+    rx[2] = R.stages[l].mode;
   }
+  if (factor) {
+    factor[0] = R.level_factor[l].real();
+    factor[1] = R.level_factor[l].imag();
+  }
+  return QAOA_OK;
+}
 
-  if ((rc = record_event(c, timing, ev++))) return rc;
-  for (size_t i = 0; i < plan.size(); ++i) {
-    const SweepPlan& sp = plan[i];
-    const SetDesc& s = sets[sp.set];
-    SweepArgs a;
-    memset(&a, 0, sizeof(a));
-    a.amps = c->amps;
-    a.g = c->g;
-    a.ntiles = ntiles;
-    a.partials = c->partials;
-    a.carry = s.carry;
-    a.q = s.q;
-    uint32_t fl = exact ? kExact : 0u;
-    if (i == 0 && !from_state) {
-      fl |= kGen;
-      a.gen = make_double2(u, 0.0);
-    }
-    a.table_len = te;
-    if (sp.pre_cost >= 0) {
-      fl |= kPreCost;
-      a.table = c->d_tables + (size_t)sp.pre_cost * te;
-    }
-    if (sp.mid_cost >= 0) {
-      fl |= kMidCost;
-      a.table2 = c->d_tables + (size_t)sp.mid_cost * te;
-    }
-    if (sp.stage1 >= 0) {
-      fl |= kStage1;
-      a.rx1 = stages[sp.stage1];
-    }
-    if (sp.stage2 >= 0) {
-      fl |= kStage2;
-      a.rx2 = stages[sp.stage2];
-    }
-    const bool last = i + 1 == plan.size();
-    if (last && !exact) {
-      fl |= kScale;
-      a.scale = make_double2(final_scale.real(), final_scale.imag());
-    }
-    if (last && want_expect) fl |= kExpect;
-    a.flags = fl;
-    CUDA_TRY(launch_sweep(a, grid, c->stream));
-    ++c->last_launches;
-    c->last_bytes += ((fl & kGen) ? 16.0 : 32.0) * (double)size;
-    if ((rc = record_event(c, timing, ev++))) return rc;
+int qaoa_run_end(qaoa_ctx* c) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  return run_end(c);
+}
+
+int qaoa_exchange(int device, void* stream, int g, void* const* shards, int n_local, int p0,
+                  uint64_t y_lo, uint64_t y_hi, const double* rx, const double* factor) {
+  if (g < 1 || g > 4) return fail(QAOA_E_INVALID, "shard bits must be in [1, 4]");
+  if (!shards || !rx || !factor) return fail(QAOA_E_INVALID, "null argument");
+  if (n_local < g || p0 < 0 || p0 + g > n_local) return fail(QAOA_E_RANGE, "swapped bits out of range");
+  if (y_hi > (1ull << (n_local - g)) || y_lo > y_hi) return fail(QAOA_E_RANGE, "column range out of range");
+  CUDA_TRY(cudaSetDevice(device));
+  ExchangeArgs a;
+  memset(&a, 0, sizeof(a));
+  const int G = 1 << g;
+  for (int r = 0; r < G; ++r) {
+    if (!shards[r]) return fail(QAOA_E_INVALID, "null shard pointer");
+    a.shards[r] = (double2*)shards[r];
   }
-  if (!from_state) c->g.cmask = 0;
-  if (flips) c->g.cmask ^= local_mask(c);
-  if (want_expect) {
-    if ((rc = reduce_to_host(c, n_partials, 0, &c->expect_value))) return rc;
-    ++c->last_launches;
-    c->expect_valid = true;
-  }
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  if (timing) {
-    for (size_t i = 0; i + 1 < ev; ++i) {
-      float ms = 0.f;
-      CUDA_TRY(cudaEventElapsedTime(&ms, c->events[i], c->events[i + 1]));
-      c->times.push_back(ms);
-    }
-  }
+  a.g = g;
+  a.p0 = p0;
+  a.y_lo = y_lo;
+  a.y_hi = y_hi;
+  a.rx = RxStage{rx[0], rx[1], (int)rx[2]};
+  const std::complex<double> f = std::pow(std::complex<double>(factor[0], factor[1]), g);
+  a.scale = make_double2(f.real(), f.imag());
+  a.scale_on = !(f.real() == 1.0 && f.imag() == 0.0);
+  CUDA_TRY(launch_exchange(a, (cudaStream_t)stream));
+  return QAOA_OK;
+}
+
+int qaoa_ipc_handle(qaoa_ctx* c, void* handle64) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (!handle64) return fail(QAOA_E_INVALID, "null handle buffer");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, c->amps));
+  memcpy(handle64, &h, sizeof(h));
+  return QAOA_OK;
+}
+
+int qaoa_ipc_open(const void* handle64, int device, void** out_ptr) {
+  if (!handle64 || !out_ptr) return fail(QAOA_E_INVALID, "null argument");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  CUDA_TRY(cudaIpcOpenMemHandle(out_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return QAOA_OK;
+}
+
+int qaoa_ipc_close(void* ptr) {
+  CUDA_TRY(cudaIpcCloseMemHandle(ptr));
   return QAOA_OK;
 }
 

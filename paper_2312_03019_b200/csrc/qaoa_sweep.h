@@ -88,4 +88,17 @@ cudaError_t launch_sample_blocks(const double2* amps, int block_bits, uint64_t l
                                  cudaStream_t s);
 int reduce_grid();
 
+// fused global<->local exchange + RX of the arriving qubits (qaoa_exchange.cu)
+constexpr int kMaxShards = 16;
+struct ExchangeArgs {
+  double2* shards[kMaxShards];  // G = 2^g shard bases, valid on the launching device
+  int g;                        // global (shard) bits
+  int p0;                       // swapped local bits p0 .. p0+g-1
+  uint64_t y_lo, y_hi;          // range of y (local index without bits p0..) handled here
+  RxStage rx;                   // mode 0: exact (c, s); 1: factored form 1 (t)
+  double2 scale;                // applied after the butterflies when scale_on
+  int scale_on;
+};
+cudaError_t launch_exchange(const ExchangeArgs& a, cudaStream_t s);
+
 }  // namespace qb

@@ -25,6 +25,7 @@ a CPU shard built on the oracle.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field
 from typing import Protocol, Sequence
@@ -66,13 +67,25 @@ class ShardLayout:
             self.phys[qa], self.phys[qb] = b, a
             where[a], where[b] = qb, qa
 
-    def swap_bits(self, x: int) -> int:
-        """Apply the same bit swap to a physical index / mask."""
+    def swap_bits(self, x: int, p0: int | None = None) -> int:
+        """Apply the same bit swap (local bits p0.. <-> global bits; default the
+        top local bits) to a physical index / mask."""
         nl, g = self.n_local, self.g
-        lo = (x >> (nl - g)) & ((1 << g) - 1)
+        p0 = nl - g if p0 is None else p0
+        lo = (x >> p0) & ((1 << g) - 1)
         hi = (x >> nl) & ((1 << g) - 1)
-        x &= ~((((1 << g) - 1) << (nl - g)) | (((1 << g) - 1) << nl))
-        return x | (hi << (nl - g)) | (lo << nl)
+        x &= ~((((1 << g) - 1) << p0) | (((1 << g) - 1) << nl))
+        return x | (hi << p0) | (lo << nl)
+
+    def swap_at(self, p0: int) -> None:
+        """Global physical bits n_local+k <-> local physical bits p0+k."""
+        nl, g = self.n_local, self.g
+        where = {p: q for q, p in enumerate(self.phys)}
+        for k in range(g):
+            a, b = p0 + k, nl + k
+            qa, qb = where[a], where[b]
+            self.phys[qa], self.phys[qb] = b, a
+            where[a], where[b] = qb, qa
 
     def physical_row_masks(self, g: Graph) -> list[int]:
         """Row masks of the graph relabelled to physical bit positions."""
@@ -121,6 +134,12 @@ class CudaShard:
         self.n = n_local
         self.device = device
         self.exact = exact
+        if stream is None:  # a stream this side knows, so exchanges can be ordered on it
+            import torch
+
+            self._stream = torch.cuda.Stream(device)
+            stream = self._stream.cuda_stream
+        self.stream_ptr = stream
         self.eng = Engine(n_local, device, stream=stream)
 
     def set_graph(self, n_nodes, masks, tot_edge, x_hi):
@@ -167,6 +186,47 @@ class CudaShard:
 
     def synchronize(self):
         self.eng.call("qaoa_synchronize")
+
+    # ---- planned runs in segments + fused exchange (the product path) ----------
+    def run_begin(self, tables, cs, ss, flags: int) -> int:
+        from . import _lib
+
+        self._keep = (np.ascontiguousarray(tables, dtype=np.complex128),
+                      np.ascontiguousarray(cs, dtype=np.float64),
+                      np.ascontiguousarray(ss, dtype=np.float64))
+        t, c, s = self._keep
+        nseg = ctypes.c_int()
+        self.eng.call("qaoa_run_begin", len(c), _lib.dptr(t.view(np.float64)), _lib.dptr(c),
+                      _lib.dptr(s), int(flags), ctypes.byref(nseg))
+        return nseg.value
+
+    def run_segment(self, k: int) -> None:
+        self.eng.call("qaoa_run_segment", int(k))
+
+    def exchange_info(self, k: int):
+        """(level, rx[3], factor[2]) of the exchange after segment k, or None."""
+        from . import _lib
+
+        lvl = ctypes.c_int()
+        rx = np.zeros(3)
+        fac = np.zeros(2)
+        rc = self._lib.load().qaoa_run_exchange_info(self.eng.ptr, int(k), ctypes.byref(lvl),
+                                                     _lib.dptr(rx), _lib.dptr(fac))
+        if rc == _lib.QAOA_E_RANGE:
+            return None
+        _lib.check(rc)
+        return lvl.value, rx, fac
+
+    def run_end(self) -> None:
+        self.eng.call("qaoa_run_end")
+
+    def state_ptr(self) -> int:
+        return self.eng.state_ptr()
+
+    def ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        self.eng.call("qaoa_ipc_handle", buf)
+        return buf.raw
 
     def close(self):
         self.eng.close()
@@ -300,3 +360,139 @@ def gather_true_state(layout: ShardLayout, stored: np.ndarray, cmask: int) -> np
     logical order: true[X] = stored[phys(X) ^ cmask]."""
     idx = np.arange(stored.size, dtype=np.uint64)
     return stored[layout.logical_to_physical(idx) ^ np.uint64(cmask)]
+
+
+# --------------------------------------------------------------------------
+# the fused path: segmented shard runs + in-place exchange kernel over peer
+# pointers (qaoa_exchange), RX of the arriving qubits fused into the exchange
+# --------------------------------------------------------------------------
+def exchange_p0(g_bits: int) -> int:
+    """Local bits swapped with the global ones: the top g bits of the low set
+    S_0 (local bits 0..11), which every level finishes before its exchange."""
+    return 12 - g_bits
+
+
+def _exchange_call(device, stream, g_bits, ptrs, n_local, p0, y_lo, y_hi, rx, factor):
+    from . import _lib
+
+    arr = (ctypes.c_void_p * len(ptrs))(*[ctypes.c_void_p(int(p)) for p in ptrs])
+    rx = np.ascontiguousarray(rx, dtype=np.float64)
+    factor = np.ascontiguousarray(factor, dtype=np.float64)
+    _lib.check(_lib.load().qaoa_exchange(int(device), ctypes.c_void_p(stream), int(g_bits), arr,
+                                         int(n_local), int(p0), int(y_lo), int(y_hi),
+                                         _lib.dptr(rx), _lib.dptr(factor)))
+
+
+class PeerExchanger:
+    """All G shards in this process on one device (virtual shards): one launch
+    of the exchange kernel over the G buffers."""
+
+    def __init__(self, shards: Sequence[CudaShard]):
+        self.shards = list(shards)
+        self.ptrs = [s.state_ptr() for s in self.shards]
+
+    def exchange(self, g_bits: int, p0: int, rx, factor) -> None:
+        for s in self.shards:
+            s.synchronize()
+        import torch
+
+        s0 = self.shards[0]
+        _exchange_call(s0.device, s0.stream_ptr, g_bits, self.ptrs, s0.n, p0, 0,
+                       1 << (s0.n - g_bits), rx, factor)
+        torch.cuda.synchronize(s0.device)
+
+
+class IpcExchanger:
+    """One shard per process (one GPU each): the peers' state buffers are mapped
+    with CUDA IPC, rank r runs the exchange kernel on its 1/G of the columns with
+    P2P loads / stores over NVLink; host barriers order it against the shards'
+    sweeps."""
+
+    def __init__(self, shard: CudaShard, rank: int, world: int, group=None):
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self.shard, self.rank, self.world, self.group = shard, rank, world, group
+        handles = [None] * world
+        dist.all_gather_object(handles, shard.ipc_handle(), group=group)
+        self.ptrs, self.opened = [], []
+        for r, h in enumerate(handles):
+            if r == rank:
+                self.ptrs.append(shard.state_ptr())
+                continue
+            out = ctypes.c_void_p()
+            buf = ctypes.create_string_buffer(h, 64)
+            _lib.check(_lib.load().qaoa_ipc_open(buf, int(shard.device), ctypes.byref(out)))
+            self.ptrs.append(out.value)
+            self.opened.append(out.value)
+
+    def _barrier(self):
+        import torch.distributed as dist
+
+        dist.barrier(group=self.group)
+
+    def exchange(self, g_bits: int, p0: int, rx, factor) -> None:
+        sh = self.shard
+        cols = 1 << (sh.n - g_bits)
+        lo = cols * self.rank // self.world
+        hi = cols * (self.rank + 1) // self.world
+        sh.synchronize()
+        self._barrier()  # every shard finished the segment before anyone reads it
+        import torch
+
+        _exchange_call(sh.device, sh.stream_ptr, g_bits, self.ptrs, sh.n, p0, lo, hi, rx, factor)
+        torch.cuda.synchronize(sh.device)
+        self._barrier()  # every write into my shard landed before my next sweep
+
+    def close(self) -> None:
+        from . import _lib
+
+        for p in self.opened:
+            _lib.load().qaoa_ipc_close(ctypes.c_void_p(p))
+        self.opened = []
+
+
+def simulate_sharded_fused(g: Graph, params: QaoaParams, shards: Sequence[CudaShard], exchanger,
+                           g_bits: int, exact: bool = False, expect: bool = False,
+                           timing: bool = False, layout: ShardLayout | None = None) -> ShardLayout:
+    """p levels on a state sharded 2^g_bits ways with the fused schedule: per
+    level the shard-local sweeps of the fast plan (level-boundary sweeps merged
+    as on one GPU) stop once after the low set S_0 for ONE exchange that swaps
+    the global qubits with S_0's top g bits and applies this level's RX to the
+    arriving ones (R - 1 local sweeps + 1 exchange pass per level for R local
+    qubit sets).  ``shards`` are those owned by this process."""
+    from . import _lib
+
+    n_total = g.n
+    layout = layout or ShardLayout(n_total, g_bits)
+    nl = layout.n_local
+    if g_bits < 1 or g_bits > 4 or nl < 12:
+        raise ValueError("fused sharding needs 1..4 shard bits and >= 12 local qubits")
+    p0 = exchange_p0(g_bits)
+    tables, cs, ss = level_arrays(g, params)
+
+    def push_graph():
+        masks = layout.physical_row_masks(g)
+        for sh in shards:
+            sh.set_graph(n_total, masks, g.tot_edge, sh.rank << nl)
+
+    push_graph()
+    flags = _lib.RUN_SHARDED | (_lib.RUN_EXACT if exact else 0) | \
+        (_lib.RUN_EXPECTATION if expect else 0) | (_lib.RUN_TIMING if timing else 0)
+    nseg = [sh.run_begin(tables, cs, ss, flags) for sh in shards][0]
+    for k in range(nseg):
+        for sh in shards:
+            sh.run_segment(k)
+        info = shards[0].exchange_info(k)
+        if info is None:
+            continue
+        _, rx, factor = info
+        exchanger.exchange(g_bits, p0, rx, factor)
+        for sh in shards:
+            sh.set_cmask(layout.swap_bits(sh.get_cmask(), p0))
+        layout.swap_at(p0)
+        push_graph()
+    for sh in shards:
+        sh.run_end()
+    return layout

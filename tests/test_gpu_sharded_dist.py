@@ -16,13 +16,16 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_torchrun_sharded_bench(world):
+@pytest.mark.parametrize("world,exchange", [(2, "ipc"), (4, "ipc"), (2, "nccl"), (4, "nccl")])
+def test_torchrun_sharded_bench(world, exchange):
+    """ipc: the fused exchange kernel with the peers' shards mapped by CUDA IPC
+    (here all on one device); nccl: the staging path."""
     n, p = 22, 3
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world),
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + (10 if exchange == "ipc" else 0)),
            os.path.join(ROOT, "bench.py"), "--gpus", str(world), "--steps", "2", "--warmup", "3",
-           "--qubits", str(n), "--levels", str(p), "--dist-backend", "gloo", "--share-device"]
+           "--qubits", str(n), "--levels", str(p), "--dist-backend", "gloo", "--share-device",
+           "--exchange", exchange]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])

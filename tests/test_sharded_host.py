@@ -123,3 +123,135 @@ def test_gloo_sharded_matches_unsharded(world, n, p):
     from oracle import oracle as O
 
     assert e == pytest.approx(O.expectation(n, g.row_mask, ref), rel=1e-10)
+
+
+# ---- the fused path (segmented runs + in-place exchange with RX of the
+# arriving qubits): host driver against the oracle, exchange restated in numpy
+class NumpyExchanger:
+    """In-process stand-in for PeerExchanger: oracle.fused_exchange_numpy over
+    the G oracle shards' arrays."""
+
+    def __init__(self, shards):
+        self.shards = shards
+
+    def exchange(self, g_bits, p0, rx, factor):
+        from oracle.oracle import fused_exchange_numpy
+
+        assert factor[0] == 1.0 and factor[1] == 0.0  # oracle shards run exact levels
+        fused_exchange_numpy([s.tensor().numpy() for s in self.shards], g_bits, p0, rx)
+
+
+class GatherExchanger:
+    """Multi-process stand-in for IpcExchanger over gloo: gather every shard,
+    run the same in-place exchange, keep this rank's shard."""
+
+    def __init__(self, shard, rank, world):
+        self.shard, self.rank, self.world = shard, rank, world
+
+    def exchange(self, g_bits, p0, rx, factor):
+        from oracle.oracle import fused_exchange_numpy
+
+        parts = [torch.zeros_like(self.shard.tensor()) for _ in range(self.world)]
+        dist.all_gather(parts, self.shard.tensor())
+        arrs = [t.numpy().copy() for t in parts]
+        fused_exchange_numpy(arrs, g_bits, p0, rx)
+        self.shard.tensor().numpy()[:] = arrs[self.rank]
+
+
+def test_layout_swap_at_p0():
+    L = ShardLayout(16, 2)
+    p0 = 10
+    L.swap_at(p0)
+    assert L.phys[10:12] == [14, 15] and L.phys[14:16] == [10, 11]
+    assert L.swap_bits(1 << 10, p0) == 1 << 14 and L.swap_bits(1 << 15, p0) == 1 << 11
+    x = 0b10_0000_11_0000000000
+    assert L.swap_bits(L.swap_bits(x, p0), p0) == x
+
+
+def test_fused_exchange_numpy_is_transpose_plus_rx():
+    """The numpy restatement moves (shard r, local (y, h)) to (shard h, local (y, r))
+    and with c = 1, s = 0 does nothing else."""
+    from oracle.oracle import fused_exchange_numpy
+
+    G, n, p0, g = 4, 8, 3, 2
+    rng = np.random.default_rng(0)
+    arrs = [rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n) for _ in range(G)]
+    old = [a.copy() for a in arrs]
+    fused_exchange_numpy(arrs, g, p0, np.array([1.0, 0.0, 0.0]))
+    for r in range(G):
+        for x in range(1 << n):
+            h = (x >> p0) & (G - 1)
+            y_lo, y_hi = x & ((1 << p0) - 1), x >> (p0 + g)
+            dst = y_lo | (r << p0) | (y_hi << (p0 + g))
+            assert arrs[h][dst] == old[r][x]
+
+
+@pytest.mark.parametrize("n,gbits,p", [(13, 1, 3), (14, 2, 2), (15, 3, 2)])
+def test_fused_virtual_shards_cpu(n, gbits, p):
+    from oracle import oracle as O
+    from oracle.oracle import OracleShard
+    from paper_2312_03019_b200.sharded import simulate_sharded_fused
+
+    g = Q.random_regular_graph(n, 3, seed=n + 1) if n % 2 == 0 else Q.erdos_renyi_graph(n, 0.4, n)
+    pr = Q.params_from_seed(p, n)
+    shards = [OracleShard(n - gbits, r) for r in range(1 << gbits)]
+    layout = simulate_sharded_fused(g, pr, shards, NumpyExchanger(shards), gbits, exact=True)
+    stored = np.concatenate([s.tensor().numpy() for s in shards])
+    true = gather_true_state(layout, stored, 0)
+    ref = reference_state(g, pr)
+    assert np.max(np.abs(true - ref)) <= 1e-12
+    # one swap per level: an odd level count leaves S_0's top qubits global
+    assert (layout.phys != list(range(n))) == (p % 2 == 1)
+    assert sharded_expectation(shards) == pytest.approx(O.expectation(n, g.row_mask, ref),
+                                                        rel=1e-10)
+
+
+def _fused_worker(rank, world, port, n, gbits, p, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import OracleShard
+        from paper_2312_03019_b200.sharded import simulate_sharded_fused
+
+        g = Q.random_regular_graph(n, 3, seed=5)
+        pr = Q.params_from_seed(p, 4)
+        shard = OracleShard(n - gbits, rank)
+        layout = simulate_sharded_fused(g, pr, [shard], GatherExchanger(shard, rank, world), gbits,
+                                        exact=True)
+        parts = [None] * world
+        dist.all_gather_object(parts, {rank: shard.expectation()})
+        merged = {}
+        for d in parts:
+            merged.update(d)
+        e = float(sum(merged[r] for r in sorted(merged)))
+        shards = [torch.zeros_like(shard.tensor()) for _ in range(world)]
+        dist.all_gather(shards, shard.tensor())
+        if rank == 0:
+            stored = np.concatenate([t.numpy() for t in shards])
+            out.put((gather_true_state(layout, stored, 0), e))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,p", [(2, 14, 3), (4, 14, 2)])
+def test_gloo_fused_sharded_matches_unsharded(world, n, p):
+    gbits = world.bit_length() - 1
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, n, gbits, p, q))
+             for r in range(world)]
+    for pr_ in procs:
+        pr_.start()
+    true, e = q.get(timeout=180)
+    for pr_ in procs:
+        pr_.join(timeout=120)
+        assert pr_.exitcode == 0
+    g = Q.random_regular_graph(n, 3, seed=5)
+    pr = Q.params_from_seed(p, 4)
+    ref = reference_state(g, pr)
+    assert np.max(np.abs(true - ref)) <= 1e-12
+    from oracle import oracle as O
+
+    assert e == pytest.approx(O.expectation(n, g.row_mask, ref), rel=1e-10)
