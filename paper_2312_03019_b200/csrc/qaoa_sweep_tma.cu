@@ -493,7 +493,8 @@ void set_sweep_impl(int v) { g_impl = v; }
 // Measured on B200 at N=30 (tools/sweep_probe.cu, ms per sweep):
 //   launch-control (kGen) sweep      v4 4.48 | TMA in/out 4.10          -> 2
 //   merged sweep of the top set      v4 7.85 | TMA-fed 7.96 | in/out 7.57 -> 2
-//   (tile spans > 256 MB: 512 DRAM pages per tile, L2 prefetch hurts)
+//   (C = 3, tile spans > 256 MB: 512 DRAM pages per tile, L2 prefetch hurts;
+//   at N=33 the C = 5 top set is faster one tile per CTA: 50.1 vs 53.1 ms)
 //   everything else                  v4 + L2 prefetch is fastest        -> 0
 int sweep_impl(const SweepArgs& a) {
   if ((a.flags & kExact) || a.carry == 11 || a.ntiles < 1) return 0;
@@ -501,7 +502,7 @@ int sweep_impl(const SweepArgs& a) {
   if (env != 3) return env;
   if (a.flags & kGen) return 2;
   const bool wide_span = a.carry < 12 && a.q + 12 - a.carry + 4 > 28;
-  if ((a.flags & kStage2) && wide_span) return 2;
+  if ((a.flags & kStage2) && wide_span && a.carry == 3) return 2;
   return 0;
 }
 

@@ -187,9 +187,15 @@ int main(int argc, char** argv) {
       {"last S2 (expect)", 12 - m, 12 + (high - m), kStage1 | kScale | kExpect},
   };
   const double bytes = 32.0 * (double)size;
-  if (argc > 4) {  // sweep_probe N REPS IMPL KIND: one kind, one impl (for ncu)
+  if (argc > 4) {  // sweep_probe N REPS IMPL KIND | custom C q FLAGS: one kind, one impl
     const int impl = atoi(argv[3]);
-    const Kind& k = kinds[atoi(argv[4])];
+    Kind custom{"custom", 0, 0, 0u};
+    if (strcmp(argv[4], "custom") == 0 && argc > 7) {
+      custom.carry = atoi(argv[5]);
+      custom.q = atoi(argv[6]);
+      custom.flags = (uint32_t)strtol(argv[7], nullptr, 0);
+    }
+    const Kind& k = strcmp(argv[4], "custom") == 0 ? custom : kinds[atoi(argv[4])];
     set_sweep_impl(impl);
     SweepArgs a;
     memset(&a, 0, sizeof(a));
@@ -198,7 +204,8 @@ int main(int argc, char** argv) {
     a.rx1 = RxStage{0.3, 0.0, 1}; a.rx2 = RxStage{-0.2, 0.0, 1};
     a.table_len = E + 1; a.flags = k.flags;
     const float t = time_sweep(a, grid, reps);
-    printf("%s impl %d: %.3f ms (%.0f GB/s)\n", k.name, impl, t, bytes / t / 1e6);
+    printf("%s C=%d q=%d flags=0x%x impl %d: %.3f ms (%.0f GB/s)\n", k.name, k.carry, k.q, k.flags, impl, t,
+           bytes / t / 1e6);
     return 0;
   }
   printf("n=%d E=%d grid=%d\n", n, E, grid);
