@@ -1119,7 +1119,7 @@ int qaoa_build_cut_table(qaoa_ctx* c) {
   }
   GraphDev gt = c->g;
   gt.cmask = 0;  // the table is of true indices, independent of the state
-  if (c->n >= 12) CUDA_TRY(launch_cut_table_tiles(c->cut_table, bytes_per, c->n, gt, c->stream));
+  if (c->n >= 11) CUDA_TRY(launch_cut_table_warps(c->cut_table, bytes_per, c->n, gt, c->stream));
   else CUDA_TRY(launch_cut_table(c->cut_table, bytes_per, c->n, gt, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   return QAOA_OK;

@@ -205,62 +205,6 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   }
 }
 
-// ---- K1: the cut-table builder (CompressedCostPlan.cut_counts, cost.py:88-99)
-// One CTA per 4096 consecutive states (the C = 12 tile): warp 0 builds the cut
-// basis of the tile, every thread derives the exact counts of 16 consecutive
-// states (mapping M0: registers = tile bits 0..3) and writes them as one
-// 16-byte (uint8) or two 16-byte (uint16) streaming stores -- 512 contiguous
-// bytes per warp instruction.
-template <bool WIDE, typename T>
-__global__ void __launch_bounds__(kThreads) cut_table_tile_kernel(T* __restrict__ table,
-                                                                  const SweepArgs a) {
-  __shared__ CutBasis cb;
-  const uint64_t base = (uint64_t)blockIdx.x << 12;
-  if (threadIdx.x < 32) cut_basis<WIDE, 12>(a, base, 0, &cb);
-  __syncthreads();
-  int c[16];
-  cut16<0>(&cb, c, threadIdx.x);
-  const uint64_t first = base + (uint64_t)tile_index<0>(threadIdx.x, 0);  // 16 consecutive states
-  if (sizeof(T) == 1) {
-    uint4 o;
-    o.x = (uint32_t)c[0] | ((uint32_t)c[1] << 8) | ((uint32_t)c[2] << 16) | ((uint32_t)c[3] << 24);
-    o.y = (uint32_t)c[4] | ((uint32_t)c[5] << 8) | ((uint32_t)c[6] << 16) | ((uint32_t)c[7] << 24);
-    o.z = (uint32_t)c[8] | ((uint32_t)c[9] << 8) | ((uint32_t)c[10] << 16) | ((uint32_t)c[11] << 24);
-    o.w = (uint32_t)c[12] | ((uint32_t)c[13] << 8) | ((uint32_t)c[14] << 16) | ((uint32_t)c[15] << 24);
-    __stcs(reinterpret_cast<uint4*>(table + first), o);
-  } else {
-    uint4 o0, o1;
-    o0.x = (uint32_t)c[0] | ((uint32_t)c[1] << 16);
-    o0.y = (uint32_t)c[2] | ((uint32_t)c[3] << 16);
-    o0.z = (uint32_t)c[4] | ((uint32_t)c[5] << 16);
-    o0.w = (uint32_t)c[6] | ((uint32_t)c[7] << 16);
-    o1.x = (uint32_t)c[8] | ((uint32_t)c[9] << 16);
-    o1.y = (uint32_t)c[10] | ((uint32_t)c[11] << 16);
-    o1.z = (uint32_t)c[12] | ((uint32_t)c[13] << 16);
-    o1.w = (uint32_t)c[14] | ((uint32_t)c[15] << 16);
-    __stcs(reinterpret_cast<uint4*>(table + first), o0);
-    __stcs(reinterpret_cast<uint4*>(table + first) + 1, o1);
-  }
-}
-
-cudaError_t launch_cut_table_tiles(void* table, int bytes_per, int n_local, const GraphDev& g,
-                                   cudaStream_t s) {
-  SweepArgs a;
-  memset(&a, 0, sizeof(a));
-  a.g = g;
-  a.g.cmask = 0;
-  const unsigned grid = 1u << (n_local - 12);
-  const bool wide = g.n_nodes > 32;
-  if (bytes_per == 1) {
-    if (wide) cut_table_tile_kernel<true, uint8_t><<<grid, kThreads, 0, s>>>((uint8_t*)table, a);
-    else cut_table_tile_kernel<false, uint8_t><<<grid, kThreads, 0, s>>>((uint8_t*)table, a);
-  } else {
-    if (wide) cut_table_tile_kernel<true, uint16_t><<<grid, kThreads, 0, s>>>((uint16_t*)table, a);
-    else cut_table_tile_kernel<false, uint16_t><<<grid, kThreads, 0, s>>>((uint16_t*)table, a);
-  }
-  return cudaGetLastError();
-}
-
 size_t sweep_smem_bytes(int) { return (size_t)kSlots * sizeof(double2); }
 
 template <bool WIDE, int C, int FLOW>

@@ -68,8 +68,8 @@ cudaError_t launch_sum_partials(const double* partials, int n, double* out, int 
                                 cudaStream_t s);
 cudaError_t launch_cut_table(void* table, int bytes_per, int n_local, const GraphDev& g,
                              cudaStream_t s);
-cudaError_t launch_cut_table_tiles(void* table, int bytes_per, int n_local, const GraphDev& g,
-                                   cudaStream_t s);
+cudaError_t launch_cut_table_warps(void* table, int bytes_per, int n_local, const GraphDev& g,
+                                   cudaStream_t s);  // qaoa_cut_table.cu (n_local >= 11)
 cudaError_t launch_pack_chunks(const double2* amps, int n_local, int g, const int* local_bits,
                                double2* dst, cudaStream_t s);
 cudaError_t launch_unpack_chunks(double2* amps, int n_local, int g, const int* local_bits,

@@ -122,10 +122,43 @@ def test_dense_graph_uint16_cut_table(oracle):
         assert np.max(np.abs(f.amps - ref)) <= AMP_TOL
 
 
-@pytest.mark.parametrize("n", [4, 10, 13, 20, 25])
+@pytest.mark.parametrize("n", [4, 10, 11, 12, 13, 20, 25])
 def test_cut_table_bit_exact(oracle, n):
     g = Q.random_regular_graph(n, 3, seed=7) if n % 2 == 0 else Q.erdos_renyi_graph(n, 0.5, 7)
     assert np.array_equal(Q.build_cut_table(g), oracle.cut_counts(n, g.row_mask))
+
+
+def _cut_counts_numpy(row_mask, xs):
+    """C(x) = sum_i popcount(row_mask[i] & (bcast(x_i) ^ x)) (cost.py:55-63, 88-99)."""
+    c = np.zeros(xs.size, dtype=np.int64)
+    for i, m in enumerate(row_mask):
+        b = np.uint64(0) - ((xs >> np.uint64(i)) & np.uint64(1))
+        c += np.bitwise_count(np.uint64(m) & (b ^ xs)).astype(np.int64)
+    return c
+
+
+@pytest.mark.parametrize("n_nodes,dense", [(34, False), (40, True)])
+def test_cut_table_wide_graph_fixed_high_bits(n_nodes, dense):
+    """Graphs beyond 32 nodes (64-bit masks) on a 2^20 local index space with the
+    high node bits fixed by x_hi (the table of one shard): uint8 and uint16."""
+    from paper_2312_03019_b200 import _lib
+
+    g = Q.erdos_renyi_graph(n_nodes, 0.5, seed=3) if dense else Q.random_regular_graph(n_nodes, 3, 5)
+    nl = 20
+    rng = np.random.default_rng(n_nodes)
+    eng = Q.Engine(nl)
+    try:
+        for _ in range(2):
+            x_hi = int(rng.integers(0, 1 << (n_nodes - nl))) << nl
+            masks = np.array(g.row_mask, dtype=np.uint64)
+            eng.call("qaoa_set_graph", n_nodes, masks.ctypes.data_as(_lib._u64p), g.tot_edge, x_hi)
+            eng.call("qaoa_build_cut_table")
+            out = np.empty(1 << nl, dtype=np.int64)
+            eng.call("qaoa_read_cut_table", 0, out.size, out.ctypes.data_as(_lib._i64p))
+            xs = np.uint64(x_hi) | np.arange(1 << nl, dtype=np.uint64)
+            assert np.array_equal(out, _cut_counts_numpy(g.row_mask, xs))
+    finally:
+        eng.close()
 
 
 def test_cut_table_invariants_large():

@@ -4,7 +4,8 @@
 // on-chip work: FP64 butterflies, shared-memory exchanges, cut counts).
 //   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -std=c++17 --expt-relaxed-constexpr \
 //        -I paper_2312_03019_b200/csrc tools/sweep_probe.cu \
-//        paper_2312_03019_b200/csrc/qaoa_sweep.cu paper_2312_03019_b200/csrc/qaoa_sweep_tma.cu -o tools/sweep_probe
+//        paper_2312_03019_b200/csrc/qaoa_sweep.cu paper_2312_03019_b200/csrc/qaoa_sweep_tma.cu \
+//        paper_2312_03019_b200/csrc/qaoa_cut_table.cu -o tools/sweep_probe
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -130,7 +131,41 @@ static int check_mode(int n_lo, int n_hi, int other) {
   return bad != 0;
 }
 
+// K1 timing: sweep_probe cut N REPS [dense]: the cut-table builder alone.
+static int cut_mode(int n, int reps, int dense) {
+  GraphDev g;
+  memset(&g, 0, sizeof(g));
+  g.n_nodes = n;
+  int E = 0;
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j) {
+      const bool e = dense ? (((i * 131 + j * 71) % 7) < (dense == 2 ? 3 : 4)) : (j == i + 1 || (j == i + n / 2 && i < n / 2));
+      if (e) { g.rm[i] |= 1ull << j; g.adj[i] |= 1ull << j; g.adj[j] |= 1ull << i; ++E; }
+    }
+  g.tot_edge = E;
+  const int bpe = E <= 255 ? 1 : 2;
+  void* t;
+  if (cudaMalloc(&t, (size_t)bpe << n) != cudaSuccess) return 1;
+  launch_cut_table_warps(t, bpe, n, g, 0);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int i = 0; i < reps; ++i) launch_cut_table_warps(t, bpe, n, g, 0);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= reps;
+  printf("cut table n=%d E=%d (%d B/state): %.3f ms = %.3e states/s = %.0f GB/s (%s)\n", n, E, bpe, ms,
+         (double)(1ull << n) / (ms * 1e-3), (double)((size_t)bpe << n) / (ms * 1e-3) / 1e9,
+         cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && strcmp(argv[1], "cut") == 0)
+    return cut_mode(atoi(argv[2]), atoi(argv[3]), argc > 4 ? atoi(argv[4]) : 0);
   if (argc > 1 && strcmp(argv[1], "check") == 0)
     return check_mode(argc > 2 ? atoi(argv[2]) : 13, argc > 3 ? atoi(argv[3]) : 24,
                       argc > 4 ? atoi(argv[4]) : 2);
