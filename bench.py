@@ -230,8 +230,9 @@ def run_sharded(args, rank: int, world: int, local: int):
     import torch.distributed as tdist
 
     import paper_2312_03019_b200 as Q
-    from paper_2312_03019_b200.sharded import (CudaShard, DistExchanger, IpcExchanger,
-                                               simulate_sharded, simulate_sharded_fused)
+    from paper_2312_03019_b200.sharded import (CudaShard, DistExchanger, IpcChunkExchanger,
+                                               IpcExchanger, simulate_sharded,
+                                               simulate_sharded_fused)
 
     if world & (world - 1):
         raise SystemExit("sharded mode needs a power-of-two GPU count")
@@ -246,7 +247,12 @@ def run_sharded(args, rank: int, world: int, local: int):
     fused = args.exchange == "ipc"
     shard = CudaShard(n - gbits, rank, device=local, exact=args.exact,
                       stream=None if fused else torch.cuda.current_stream(local).cuda_stream)
-    exch = IpcExchanger(shard, rank, world) if fused else DistExchanger(shard, rank, world)
+    if fused and args.chunks > 1:
+        exch = IpcChunkExchanger(shard, rank, world, args.chunks)
+    elif fused:
+        exch = IpcExchanger(shard, rank, world)
+    else:
+        exch = DistExchanger(shard, rank, world)
 
     def step():
         if fused:
@@ -485,6 +491,9 @@ def main():
     ap.add_argument("--exchange", choices=["ipc", "nccl"], default="ipc",
                     help="sharded runs: fused exchange kernel over CUDA-IPC peer pointers "
                          "(default) or the NCCL P2P staging path")
+    ap.add_argument("--chunks", type=int, default=4,
+                    help="sharded ipc runs: pipeline each exchange with the sweeps around it "
+                         "in this many chunks (1 = no overlap)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: one full state per rank (weak scaling) instead of sharding")
     args = ap.parse_args()

@@ -206,6 +206,17 @@ QAOA_API int qaoa_run_segment(qaoa_ctx* ctx, int k);
  * QAOA_E_RANGE when no exchange follows segment k. */
 QAOA_API int qaoa_run_exchange_info(qaoa_ctx* ctx, int k, int* level, double* rx, double* factor);
 QAOA_API int qaoa_run_end(qaoa_ctx* ctx);
+/* Sweep-level control of a planned run (pipelining a sharded exchange with the
+ * sweeps around it): sweep i belongs to `segment`, works on the tile geometry
+ * (carry, q) -- tiles of 2^carry consecutive amplitudes times the qubits
+ * q..q+11-carry (carry 12: 4096 consecutive) -- of `ntiles` tiles, numbered so
+ * that the top index bits not mixed by the sweep are the top tile-index bits.
+ * qaoa_run_sweep_range launches sweep i on tiles [tile_lo, tile_lo + count)
+ * instead of inside qaoa_run_segment (the caller runs every sweep of the
+ * segment exactly once, in order per tile). */
+QAOA_API int qaoa_run_sweep_info(qaoa_ctx* ctx, int i, int* segment, int* carry, int* q,
+                                 int64_t* ntiles);
+QAOA_API int qaoa_run_sweep_range(qaoa_ctx* ctx, int i, int64_t tile_lo, int64_t tile_count);
 
 /* ---- fused exchange + RX over shard pointers ------------------------------
  * G = 2^g shards (g <= 4) of 2^n_local amplitudes; shards[r] is a device

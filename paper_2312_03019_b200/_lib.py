@@ -83,6 +83,8 @@ SIGNATURES = {
     "qaoa_run_segment": (_c_int, [_vp, _c_int]),
     "qaoa_run_exchange_info": (_c_int, [_vp, _c_int, _ip, _dp, _dp]),
     "qaoa_run_end": (_c_int, [_vp]),
+    "qaoa_run_sweep_info": (_c_int, [_vp, _c_int, _ip, _ip, _ip, _i64p]),
+    "qaoa_run_sweep_range": (_c_int, [_vp, _c_int, ctypes.c_int64, ctypes.c_int64]),
     "qaoa_exchange": (_c_int, [_c_int, _vp, _c_int, ctypes.POINTER(_vp), _c_int, _c_int, _u64, _u64,
                                _dp, _dp]),
     "qaoa_ipc_handle": (_c_int, [_vp, _vp]),

@@ -422,57 +422,67 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
   return QAOA_OK;
 }
 
+// Launch plan sweep i on tiles [lo, lo + cnt) (cnt = 0: all tiles).
+int launch_plan_sweep(qaoa_ctx* c, int i, int64_t lo, int64_t cnt) {
+  RunState& R = c->run;
+  const uint64_t size = 1ull << c->n;
+  const int te = c->g.tot_edge + 1;
+  const double u = sqrt(1.0 / (double)(1ull << c->g.n_nodes));
+  const SweepPlan& sp = R.plan[i];
+  const SetDesc& st = R.sets[sp.set];
+  SweepArgs a;
+  memset(&a, 0, sizeof(a));
+  a.amps = c->amps;
+  a.g = c->g;
+  a.ntiles = 1ll << (c->n - 12);
+  a.tile_lo = lo;
+  a.tile_cnt = cnt;
+  a.partials = c->partials;
+  a.carry = st.carry;
+  a.q = st.q;
+  uint32_t fl = R.exact ? kExact : 0u;
+  if (i == 0 && !R.from_state) {
+    fl |= kGen;
+    a.gen = make_double2(u, 0.0);
+  }
+  a.table_len = te;
+  if (sp.pre_cost >= 0) {
+    fl |= kPreCost;
+    a.table = c->d_tables + (size_t)sp.pre_cost * te;
+  }
+  if (sp.mid_cost >= 0) {
+    fl |= kMidCost;
+    a.table2 = c->d_tables + (size_t)sp.mid_cost * te;
+  }
+  if (sp.stage1 >= 0) {
+    fl |= kStage1;
+    a.rx1 = R.stages[sp.stage1];
+  }
+  if (sp.stage2 >= 0) {
+    fl |= kStage2;
+    a.rx2 = R.stages[sp.stage2];
+  }
+  const bool last = i + 1 == (int)R.plan.size();
+  if (last && !R.exact) {
+    fl |= kScale;
+    a.scale = make_double2(R.final_scale.real(), R.final_scale.imag());
+  }
+  if (last && R.expect_fused) fl |= kExpect;
+  a.flags = fl;
+  CUDA_TRY(launch_sweep(a, R.grid, c->stream));
+  ++c->last_launches;
+  const double frac = cnt ? (double)cnt / (double)a.ntiles : 1.0;
+  c->last_bytes += ((fl & kGen) ? 16.0 : 32.0) * (double)size * frac;
+  return QAOA_OK;
+}
+
 int run_segment(qaoa_ctx* c, int k) {
   RunState& R = c->run;
   if (!R.active) return fail(QAOA_E_STATE, "no planned run (qaoa_run_begin)");
   if (k < 0 || k + 1 >= (int)R.seg_start.size()) return fail(QAOA_E_RANGE, "segment out of range");
-  const uint64_t size = 1ull << c->n;
-  const int te = c->g.tot_edge + 1;
-  const double u = sqrt(1.0 / (double)(1ull << c->g.n_nodes));
   int rc;
   for (int i = R.seg_start[k]; i < R.seg_start[k + 1]; ++i) {
-    const SweepPlan& sp = R.plan[i];
-    const SetDesc& st = R.sets[sp.set];
-    SweepArgs a;
-    memset(&a, 0, sizeof(a));
-    a.amps = c->amps;
-    a.g = c->g;
-    a.ntiles = 1ll << (c->n - 12);
-    a.partials = c->partials;
-    a.carry = st.carry;
-    a.q = st.q;
-    uint32_t fl = R.exact ? kExact : 0u;
-    if (i == 0 && !R.from_state) {
-      fl |= kGen;
-      a.gen = make_double2(u, 0.0);
-    }
-    a.table_len = te;
-    if (sp.pre_cost >= 0) {
-      fl |= kPreCost;
-      a.table = c->d_tables + (size_t)sp.pre_cost * te;
-    }
-    if (sp.mid_cost >= 0) {
-      fl |= kMidCost;
-      a.table2 = c->d_tables + (size_t)sp.mid_cost * te;
-    }
-    if (sp.stage1 >= 0) {
-      fl |= kStage1;
-      a.rx1 = R.stages[sp.stage1];
-    }
-    if (sp.stage2 >= 0) {
-      fl |= kStage2;
-      a.rx2 = R.stages[sp.stage2];
-    }
-    const bool last = i + 1 == (int)R.plan.size();
-    if (last && !R.exact) {
-      fl |= kScale;
-      a.scale = make_double2(R.final_scale.real(), R.final_scale.imag());
-    }
-    if (last && R.expect_fused) fl |= kExpect;
-    a.flags = fl;
-    CUDA_TRY(launch_sweep(a, R.grid, c->stream));
-    ++c->last_launches;
-    c->last_bytes += ((fl & kGen) ? 16.0 : 32.0) * (double)size;
+    if ((rc = launch_plan_sweep(c, i, 0, 0))) return rc;
     if ((rc = record_event(c, R.timing, R.ev++))) return rc;
   }
   return QAOA_OK;
@@ -901,6 +911,34 @@ int qaoa_run_end(qaoa_ctx* c) {
   int rc = check_ctx(c);
   if (rc) return rc;
   return run_end(c);
+}
+
+int qaoa_run_sweep_info(qaoa_ctx* c, int i, int* segment, int* carry, int* q, int64_t* ntiles) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  const RunState& R = c->run;
+  if (!R.active) return fail(QAOA_E_STATE, "no planned run (qaoa_run_begin)");
+  if (i < 0 || i >= (int)R.plan.size()) return fail(QAOA_E_RANGE, "sweep out of range");
+  int k = 0;
+  while (k + 1 < (int)R.seg_start.size() && R.seg_start[k + 1] <= i) ++k;
+  const SetDesc& st = R.sets[R.plan[i].set];
+  if (segment) *segment = k;
+  if (carry) *carry = st.carry;
+  if (q) *q = st.q;
+  if (ntiles) *ntiles = 1ll << (c->n - 12);
+  return QAOA_OK;
+}
+
+int qaoa_run_sweep_range(qaoa_ctx* c, int i, int64_t tile_lo, int64_t tile_count) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  const RunState& R = c->run;
+  if (!R.active) return fail(QAOA_E_STATE, "no planned run (qaoa_run_begin)");
+  if (i < 0 || i >= (int)R.plan.size()) return fail(QAOA_E_RANGE, "sweep out of range");
+  const int64_t nt = 1ll << (c->n - 12);
+  if (tile_lo < 0 || tile_count < 1 || tile_lo + tile_count > nt)
+    return fail(QAOA_E_RANGE, "tile range out of range");
+  return launch_plan_sweep(c, i, tile_lo, tile_count);
 }
 
 int qaoa_exchange(int device, void* stream, int g, void* const* shards, int n_local, int p0,

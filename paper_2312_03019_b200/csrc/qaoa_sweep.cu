@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   const int tid = threadIdx.x;
   const int q = a.q;
   const uint64_t Q = 1ull << (C >= 12 ? 0 : q);
-  const uint64_t tile = blockIdx.x;
+  const uint64_t tile = (uint64_t)a.tile_lo + blockIdx.x;
   TileCtx tc;
   {
     const int low_bits = C >= 12 ? 0 : q - C;  // non-tile ranges [C, q) and [q + 12 - C, n)
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
 #pragma unroll
     for (int r = 0; r < kRegs; ++r) v[r] = a.gen;
   } else {
-    if (a.pf_dist > 0 && tile + a.pf_dist < (uint64_t)a.ntiles) {
+    if (a.pf_dist > 0 && tile + a.pf_dist < (uint64_t)(a.tile_lo + (a.tile_cnt ? a.tile_cnt : a.ntiles))) {
       if (!a.pf_tensor) {
         prefetch_tile_l2<C, kThreads>(amps, tile_base<C>(tile + a.pf_dist, q), Q, tid);
       } else if (tid == 0) {
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   }
   if (flags & kExpect) {
     const double t = block_sum<kThreads>(acc, red_scratch);
-    if (threadIdx.x == 0) a.partials[blockIdx.x] = t;
+    if (threadIdx.x == 0) a.partials[tile] = t;
   }
 }
 
@@ -276,6 +276,7 @@ static int pf_distance(const SweepArgs& a) {
 cudaError_t launch_sweep(const SweepArgs& a0, int grid, cudaStream_t stream) {
   if (sweep_uses_tma(a0)) return launch_sweep_tma(a0, stream);
   SweepArgs a = a0;
+  if (a.tile_cnt) grid = (int)a.tile_cnt;
   if (a.pf_dist == 0) a.pf_dist = pf_distance(a);
   if (a.pf_dist > 0) {
     static int tens = -1;

@@ -27,7 +27,9 @@ struct SweepArgs {
   const double2* table2; // even phase-table entries (E+1) of the mid cost step
   double* partials;      // [grid] block partial sums (kExpect)
   GraphDev g;
-  int64_t ntiles;        // 2^(n_local - 12)
+  int64_t ntiles;        // 2^(n_local - 12): the tile geometry of the state
+  int64_t tile_lo;       // this launch covers tiles [tile_lo, tile_lo + tile_cnt)
+  int64_t tile_cnt;      // 0 = all ntiles
   int carry;             // C: tile bits 0..C-1 = physical bits 0..C-1 (12 = low sweep)
   int q;                 // tile bits C..11 = physical bits q..q+11-C (the mixed qubits)
   RxStage rx1, rx2;

@@ -161,7 +161,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
   const uint64_t Q = 1ull << (C >= 12 ? 0 : q);
   const bool gen = flags & kGen;
   const bool need_cut = flags & (kPreCost | kMidCost | kExpect);
-  const uint64_t ntiles = (uint64_t)a.ntiles;
+  // tiles [lo, lo + ntiles) of the 2^(n-12) (a.ntiles) of the state; `tile` below is
+  // the index inside the range
+  const uint64_t lo = (uint64_t)a.tile_lo;
+  const uint64_t ntiles = a.tile_cnt ? (uint64_t)a.tile_cnt : (uint64_t)a.ntiles;
   const uint64_t stride = gridDim.x;
 
   ThreadSlots ts;
@@ -193,8 +196,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
     for (int i = 0; i < 4; ++i) mbar_init(&full[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (!gen) {
-      issue_half<C>(ta, land, &full[0], blockIdx.x, 0);
-      issue_half<C>(ta, land + kTile / 2, &full[2], blockIdx.x, 1);
+      issue_half<C>(ta, land, &full[0], lo + blockIdx.x, 0);
+      issue_half<C>(ta, land + kTile / 2, &full[2], lo + blockIdx.x, 1);
     }
   }
   __syncthreads();
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
         tile = blockIdx.x + (uint64_t)(2 * j + grp) * stride;
       }
       if (tile >= ntiles) break;
-      if (need_cut && tid < 32) cut_basis<WIDE, C>(a, tile_base<C>(tile, q), q, cb);
+      if (need_cut && tid < 32) cut_basis<WIDE, C>(a, tile_base<C>(lo + tile, q), q, cb);
 #pragma unroll
       for (int r = 0; r < kRegs; ++r) v[r] = a.gen;
       group_bar(bar_id);  // cut basis published; WAR on the exchange buffer / next_tile
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
       // the other group's next tile (allocated here, published before the
       // half-0 barrier; an allocation is never dropped: past the end, all are)
       if (tid == 0) next_tile[grp ^ 1] = DYN ? stride + atomicAdd(ctr, 1ull) : tile + stride;
-      if (need_cut && tid < 32) cut_basis<WIDE, C>(a, tile_base<C>(tile, q), q, cb);
+      if (need_cut && tid < 32) cut_basis<WIDE, C>(a, tile_base<C>(lo + tile, q), q, cb);
       uint64_t nxt = 0;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -249,14 +252,14 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
         }
         uint64_t* bar = &full[2 * h + (grp ^ 1)];
         if (!last) {
-          if (tid == 0) issue_half<C>(ta, land + h * (kTile / 2), bar, nxt, h);
+          if (tid == 0) issue_half<C>(ta, land + h * (kTile / 2), bar, lo + nxt, h);
         } else if (h == 0 && tid == 0) {
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
         }
       }
     }
     TileCtx tc;
-    tc.base = tile_base<C>(tile, q);
+    tc.base = tile_base<C>(lo + tile, q);
     tc.tb2 = tb2;
     tc.tb1 = tb1;
     double acc = 0.0;
@@ -281,14 +284,14 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
           for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
         }
         if (flags & kExpect) acc += expect_acc<2>(v, cb, tid);
-        finish_tile<C, 2, TS>(ta, tc, Q, v, buf, tid, bar_id, tile, 0);
+        finish_tile<C, 2, TS>(ta, tc, Q, v, buf, tid, bar_id, lo + tile, 0);
       } else {
         if (flags & kScale) {
 #pragma unroll
           for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
         }
         if (flags & kExpect) acc += expect_acc<1>(v, cb, tid);
-        finish_tile<C, 1, TS>(ta, tc, Q, v, buf, tid, bar_id, tile, 0);
+        finish_tile<C, 1, TS>(ta, tc, Q, v, buf, tid, bar_id, lo + tile, 0);
       }
     } else {
       // ---- high set: G2 (+ tile bit 3), G1 [, cost, G1 (+ tile bit 3), G2]
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
         for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
       }
       if (flags & kExpect) acc += expect_acc<last_m>(v, cb, tid, sk);
-      finish_tile<C, last_m, TS>(ta, tc, Q, v, buf, tid, bar_id, tile, sk);
+      finish_tile<C, last_m, TS>(ta, tc, Q, v, buf, tid, bar_id, lo + tile, sk);
     }
     if (flags & kExpect) {
       // per-tile partial (fixed shuffle tree, warps in order): the sum over
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
         double t = 0.0;
 #pragma unroll
         for (int w = 0; w < kThreads / 32; ++w) t += gred[grp][w];
-        a.partials[tile] = t;
+        a.partials[lo + tile] = t;
       }
     }
   }
@@ -509,9 +512,10 @@ int sweep_impl(const SweepArgs& a) {
 bool sweep_uses_tma(const SweepArgs& a) { return sweep_impl(a) != 0; }
 
 int sweep_grid(const SweepArgs& a) {
-  if (!sweep_uses_tma(a)) return (int)a.ntiles;
+  const int64_t cnt = a.tile_cnt ? a.tile_cnt : a.ntiles;
+  if (!sweep_uses_tma(a)) return (int)cnt;
   const int sms = num_sms();
-  return a.ntiles < sms ? (int)a.ntiles : sms;
+  return cnt < sms ? (int)cnt : sms;
 }
 
 cudaError_t launch_sweep_tma(const SweepArgs& a, cudaStream_t s) {

@@ -220,6 +220,28 @@ class CudaShard:
     def run_end(self) -> None:
         self.eng.call("qaoa_run_end")
 
+    def sweep_info(self, i: int):
+        """(segment, carry, q, ntiles) of plan sweep i, or None past the end."""
+        from . import _lib
+
+        seg, carry, q = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        nt = ctypes.c_int64()
+        rc = self._lib.load().qaoa_run_sweep_info(self.eng.ptr, int(i), ctypes.byref(seg),
+                                                  ctypes.byref(carry), ctypes.byref(q),
+                                                  ctypes.byref(nt))
+        if rc == _lib.QAOA_E_RANGE:
+            return None
+        _lib.check(rc)
+        return seg.value, carry.value, q.value, nt.value
+
+    def run_sweep_range(self, i: int, lo: int, count: int) -> None:
+        self.eng.call("qaoa_run_sweep_range", int(i), int(lo), int(count))
+
+    @property
+    def stream(self):
+        """The torch stream the engine launches on (created by this shard)."""
+        return self._stream
+
     def state_ptr(self) -> int:
         return self.eng.state_ptr()
 
@@ -402,6 +424,46 @@ class PeerExchanger:
         torch.cuda.synchronize(s0.device)
 
 
+class PeerChunkExchanger(PeerExchanger):
+    """Virtual shards in one process, pipelined: exchange chunk t runs on its own
+    high-priority stream as soon as every shard's chunk t of the preceding sweep
+    is done (stream events, no host waits), and each shard's following sweep on
+    chunk t waits only for that exchange chunk."""
+
+    def __init__(self, shards, n_chunks: int):
+        import torch
+
+        super().__init__(shards)
+        self.n_chunks = n_chunks
+        dev = self.shards[0].device
+        self.xstream = torch.cuda.Stream(dev, priority=-1)
+        c = n_chunks
+        self.ev_pre = [[torch.cuda.Event() for _ in range(c)] for _ in self.shards]
+        self.ev_x = [torch.cuda.Event() for _ in range(c)]
+
+    # the three phases of one pipelined exchange (see simulate_sharded_fused)
+    def after_pre_chunk(self, t: int) -> None:
+        for r, sh in enumerate(self.shards):
+            self.ev_pre[r][t].record(sh.stream)
+
+    def sync_point(self) -> None:
+        pass
+
+    def launch_chunks(self, g_bits, p0, rx, factor) -> None:
+        s0 = self.shards[0]
+        cols = 1 << (s0.n - g_bits)
+        c = self.n_chunks
+        for t in range(c):
+            for r in range(len(self.shards)):
+                self.xstream.wait_event(self.ev_pre[r][t])
+            _exchange_call(s0.device, self.xstream.cuda_stream, g_bits, self.ptrs, s0.n, p0,
+                           cols * t // c, cols * (t + 1) // c, rx, factor)
+            self.ev_x[t].record(self.xstream)
+
+    def wait_chunk(self, shard_index: int, t: int) -> None:
+        self.shards[shard_index].stream.wait_event(self.ev_x[t])
+
+
 class IpcExchanger:
     """One shard per process (one GPU each): the peers' state buffers are mapped
     with CUDA IPC, rank r runs the exchange kernel on its 1/G of the columns with
@@ -453,6 +515,64 @@ class IpcExchanger:
         self.opened = []
 
 
+class IpcChunkExchanger(IpcExchanger):
+    """One shard per process, pipelined with inter-process CUDA events: rank r's
+    exchange stream waits for EVERY rank's chunk-t event of the preceding sweep
+    before its slice of exchange chunk t, and its sweep stream waits for every
+    rank's exchange-chunk-t event before the following sweep's chunk t.  Two
+    host barriers per exchange (over a gloo group: no device synchronisation)
+    order the event records before the waits."""
+
+    def __init__(self, shard: CudaShard, rank: int, world: int, n_chunks: int, group=None):
+        import torch
+        import torch.distributed as dist
+
+        super().__init__(shard, rank, world, group)
+        self.n_chunks = n_chunks
+        self.cpu_group = dist.new_group(backend="gloo")
+        dev = shard.device
+        self.xstream = torch.cuda.Stream(dev, priority=-1)
+        mk = lambda: torch.cuda.Event(interprocess=True, enable_timing=False)  # noqa: E731
+        self.my_pre = [mk() for _ in range(n_chunks)]
+        self.my_x = [mk() for _ in range(n_chunks)]
+        # events must exist on the device before their IPC handles are taken
+        with torch.cuda.stream(shard.stream):
+            for e in self.my_pre + self.my_x:
+                e.record()
+        torch.cuda.synchronize(dev)
+        mine = ([e.ipc_handle() for e in self.my_pre], [e.ipc_handle() for e in self.my_x])
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=self.cpu_group)
+        self.pre = [[self.my_pre[t] if r == rank else torch.cuda.Event.from_ipc_handle(dev, allh[r][0][t])
+                     for t in range(n_chunks)] for r in range(world)]
+        self.x = [[self.my_x[t] if r == rank else torch.cuda.Event.from_ipc_handle(dev, allh[r][1][t])
+                   for t in range(n_chunks)] for r in range(world)]
+
+    def after_pre_chunk(self, t: int) -> None:
+        self.my_pre[t].record(self.shard.stream)
+
+    def sync_point(self) -> None:
+        import torch.distributed as dist
+
+        dist.barrier(group=self.cpu_group)
+
+    def launch_chunks(self, g_bits, p0, rx, factor) -> None:
+        sh = self.shard
+        cols = 1 << (sh.n - g_bits)
+        c, G, r = self.n_chunks, self.world, self.rank
+        for t in range(c):
+            for rr in range(G):
+                self.xstream.wait_event(self.pre[rr][t])
+            lo, hi = cols * t // c, cols * (t + 1) // c
+            _exchange_call(sh.device, self.xstream.cuda_stream, g_bits, self.ptrs, sh.n, p0,
+                           lo + (hi - lo) * r // G, lo + (hi - lo) * (r + 1) // G, rx, factor)
+            self.my_x[t].record(self.xstream)
+
+    def wait_chunk(self, shard_index: int, t: int) -> None:
+        for rr in range(self.world):
+            self.shard.stream.wait_event(self.x[rr][t])
+
+
 def simulate_sharded_fused(g: Graph, params: QaoaParams, shards: Sequence[CudaShard], exchanger,
                            g_bits: int, exact: bool = False, expect: bool = False,
                            timing: bool = False, layout: ShardLayout | None = None) -> ShardLayout:
@@ -478,21 +598,107 @@ def simulate_sharded_fused(g: Graph, params: QaoaParams, shards: Sequence[CudaSh
             sh.set_graph(n_total, masks, g.tot_edge, sh.rank << nl)
 
     push_graph()
+    pipelined = getattr(exchanger, "n_chunks", 1) > 1
     flags = _lib.RUN_SHARDED | (_lib.RUN_EXACT if exact else 0) | \
-        (_lib.RUN_EXPECTATION if expect else 0) | (_lib.RUN_TIMING if timing else 0)
+        (_lib.RUN_EXPECTATION if expect else 0) | \
+        (_lib.RUN_TIMING if timing and not pipelined else 0)
     nseg = [sh.run_begin(tables, cs, ss, flags) for sh in shards][0]
-    for k in range(nseg):
-        for sh in shards:
-            sh.run_segment(k)
-        info = shards[0].exchange_info(k)
-        if info is None:
-            continue
-        _, rx, factor = info
-        exchanger.exchange(g_bits, p0, rx, factor)
+
+    def relabel():
         for sh in shards:
             sh.set_cmask(layout.swap_bits(sh.get_cmask(), p0))
         layout.swap_at(p0)
         push_graph()
+
+    if not pipelined:
+        for k in range(nseg):
+            for sh in shards:
+                sh.run_segment(k)
+            info = shards[0].exchange_info(k)
+            if info is None:
+                continue
+            _, rx, factor = info
+            exchanger.exchange(g_bits, p0, rx, factor)
+            relabel()
+    else:
+        _run_pipelined(shards, exchanger, nseg, g_bits, p0, nl, relabel)
     for sh in shards:
         sh.run_end()
     return layout
+
+
+def _run_pipelined(shards, exchanger, nseg, g_bits, p0, nl, relabel):
+    """Exchange k overlapped with the sweeps around it, chunk by chunk: the chunk
+    of a tile is its top log2(C) local index bits, so every sweep whose qubits
+    avoid those bits splits into C contiguous tile ranges.  The sweep before
+    the exchange (S_0) runs chunk by chunk and signals each chunk; exchange
+    chunk t runs (own stream) once every shard's chunk t is done; the sweep
+    after the exchange (when its qubits avoid the chunk bits) runs chunk t once
+    exchange chunk t is done everywhere.  Everything else runs whole."""
+    C = exchanger.n_chunks
+    cb = C.bit_length() - 1
+    sweeps = []
+    i = 0
+    while True:
+        info = shards[0].sweep_info(i)
+        if info is None:
+            break
+        sweeps.append(info)
+        i += 1
+    by_seg = [[j for j, s in enumerate(sweeps) if s[0] == k] for k in range(nseg)]
+
+    def chunkable(j):
+        _, carry, q, _ = sweeps[j]
+        top = 11 if carry >= 12 else q + 11 - carry  # highest qubit the sweep mixes
+        return top < nl - cb
+
+    def ranges(j):
+        nt = sweeps[j][3]
+        return [(nt * t // C, nt * (t + 1) // C - nt * t // C) for t in range(C)]
+
+    skip_first = False
+    for k in range(nseg):
+        js = by_seg[k]
+        ex = shards[0].exchange_info(k)
+        pre = js[-1] if ex is not None else None
+        body = js[1:] if skip_first else js
+        if pre is not None:
+            body = body[:-1] if body and body[-1] == pre else body
+        for j in body:
+            for sh in shards:
+                sh.run_sweep_range(j, 0, sweeps[j][3])
+        if ex is None:
+            skip_first = False
+            continue
+        _, rx, factor = ex
+        # the sweep before the exchange, chunk by chunk (whole when it cannot split)
+        if chunkable(pre):
+            for t, (lo, cnt) in enumerate(ranges(pre)):
+                for sh in shards:
+                    sh.run_sweep_range(pre, lo, cnt)
+                exchanger.after_pre_chunk(t)
+        else:
+            for sh in shards:
+                sh.run_sweep_range(pre, 0, sweeps[pre][3])
+            for t in range(C):
+                exchanger.after_pre_chunk(t)
+        exchanger.sync_point()
+        exchanger.launch_chunks(g_bits, p0, rx, factor)
+        exchanger.sync_point()
+        relabel()  # the following sweeps see the swapped layout
+        nxt = by_seg[k + 1][0] if k + 1 < nseg and by_seg[k + 1] else None
+        # (a one-sweep segment followed by an exchange runs its sweep as that
+        # exchange's pre-sweep instead)
+        nxt_is_pre = nxt is not None and len(by_seg[k + 1]) == 1 and \
+            shards[0].exchange_info(k + 1) is not None
+        if nxt is not None and chunkable(nxt) and not nxt_is_pre:
+            for t, (lo, cnt) in enumerate(ranges(nxt)):
+                for r, sh in enumerate(shards):
+                    exchanger.wait_chunk(r, t)
+                    sh.run_sweep_range(nxt, lo, cnt)
+            skip_first = True
+        else:
+            for t in range(C):
+                for r, sh in enumerate(shards):
+                    exchanger.wait_chunk(r, t)
+            skip_first = False

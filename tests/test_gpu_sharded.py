@@ -115,3 +115,38 @@ def test_fused_virtual_shards_config_c3(oracle):
     true, e = run_virtual_fused(g, pr, 3)
     assert np.max(np.abs(true - ref)) <= 1e-12
     assert e == pytest.approx(e_full, rel=1e-10)
+
+
+# ---- pipelined: exchange chunks overlapped with the sweeps before / after
+def run_virtual_pipelined(g, pr, gbits, chunks, exact=False):
+    from paper_2312_03019_b200.sharded import PeerChunkExchanger, simulate_sharded_fused
+
+    G = 1 << gbits
+    shards = [CudaShard(g.n - gbits, r, exact=exact) for r in range(G)]
+    layout = simulate_sharded_fused(g, pr, shards, PeerChunkExchanger(shards, chunks), gbits,
+                                    exact=exact, expect=True)
+    e = sharded_expectation(shards)
+    cmask = shards[0].get_cmask()
+    stored = np.concatenate([s.tensor().cpu().numpy() for s in shards])
+    for s in shards:
+        s.close()
+    return gather_true_state(layout, stored, cmask), e
+
+
+@pytest.mark.parametrize("n,gbits,chunks,betas", [
+    (14, 1, 2, (0.4, 1.1, 2.9)),     # 2 local sets, one-sweep segments
+    (18, 2, 4, (0.3, 2.9, 1.0)),
+    (24, 3, 4, (2.95, 3.05, 0.7)),   # 3 local sets: the sweep after X is the top set (whole)
+    (27, 2, 8, (0.8, 2.2, 3.0, 0.1)),  # 3 local sets, 8 chunks
+    (25, 1, 4, (1.3, 0.6)),          # 4 local sets: both sides of X pipelined
+])
+def test_pipelined_virtual_shards_match_oracle(oracle, n, gbits, chunks, betas):
+    g = Q.random_regular_graph(n, 3, seed=n) if n % 2 == 0 else Q.erdos_renyi_graph(n, 0.3, n)
+    gammas = tuple(0.2 + 0.9 * k for k in range(len(betas)))
+    pr = Q.QaoaParams(gammas, betas)
+    ref = oracle.simulate(n, g.row_mask, g.tot_edge, gammas, betas)
+    eref = oracle.expectation(n, g.row_mask, ref)
+    for exact in (False, True):
+        true, e = run_virtual_pipelined(g, pr, gbits, chunks, exact=exact)
+        assert np.max(np.abs(true - ref)) <= 1e-12, (n, gbits, chunks, exact)
+        assert e == pytest.approx(eref, rel=1e-10)
