@@ -47,8 +47,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   __shared__ CutBasis cb;
   __shared__ double red_scratch[kThreads / 32];
   using A = Act<C>;
-  // skewed register layout for the fast C = 3 flows (select-free transposes)
-  const int sk = (FLOW != 0 && A::g0_shfl) ? lane_skew() : 0;
+  // skewed register layout for the C = 3 flows (select-free transposes; the
+  // exact butterfly is symmetric bit for bit too: its sums commute)
+  const int sk = A::g0_shfl ? lane_skew() : 0;
 
   const uint32_t flags = a.flags;
   const int tid = threadIdx.x;
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
 
   if (FLOW == 0) {
     // ---- exact: cost first (level start), then tile bits in increasing order
-    if (flags & kPreCost) apply_cost<2>(v, &cb, a.table, e);
+    if (flags & kPreCost) apply_cost<2>(v, &cb, a.table, e, tid, sk);
     if (C >= 12) {
       exchange<2, 0>(buf, ts, v);
       rx_regs2<A::g0, true>(v, r1a, r1b);
@@ -117,11 +118,11 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
       rx_regs2<A::g1, true>(v, r1a, r1b);
       exchange<1, 2>(buf, ts, v);
     } else if (A::g0_shfl) {  // tile bit 3 via the lane/register transpose
-      transpose_lane3(v);
+      transpose_lane3_sk(v);
       rx_regs2<1u, true>(v, r1a, r1b);
-      exchange<3, 1>(buf, ts, v);
+      exchange<3, 1>(buf, ts, v, sk);
       rx_regs2<A::g1, true>(v, r1a, r1b);
-      exchange<1, 2>(buf, ts, v);
+      exchange<1, 2>(buf, ts, v, sk);
     } else {
       if (A::g1) {
         exchange<2, 1>(buf, ts, v);
@@ -130,8 +131,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
       }
     }
     rx_regs2<A::g2, true>(v, r1a, r1b);
-    if (flags & kExpect) acc = expect_acc<2>(v, &cb);
-    store_tile<C, 2>(amps, tc, Q, v, flags);
+    if (flags & kExpect) acc = expect_acc<2>(v, &cb, tid, sk);
+    store_tile<C, 2>(amps, tc, Q, v, flags, sk);
   } else if (C >= 12) {
     // ---- fast, low set: G2 (loaded), G0, G1 [, cost, G1, G0, G2]
     if (flags & kPreCost) apply_cost<2>(v, &cb, a.table, e);
