@@ -255,3 +255,74 @@ def test_gloo_fused_sharded_matches_unsharded(world, n, p):
     from oracle import oracle as O
 
     assert e == pytest.approx(O.expectation(n, g.row_mask, ref), rel=1e-10)
+
+
+# ---- the pipelined schedule's host logic (no GPU): every sweep covers all its
+# tiles exactly once, chunked sweeps only around exchanges, ordered correctly
+class _PlanShard:
+    """Stand-in shard exposing a synthetic plan (segment, carry, q, ntiles)."""
+
+    def __init__(self, plan, exchanges, log, rank=0, n=24):
+        self.plan, self.exchanges, self.log, self.rank, self.n = plan, exchanges, log, rank, n
+
+    def sweep_info(self, i):
+        return self.plan[i] if i < len(self.plan) else None
+
+    def exchange_info(self, k):
+        return (k, np.zeros(3), np.array([1.0, 0.0])) if k in self.exchanges else None
+
+    def run_sweep_range(self, i, lo, cnt):
+        self.log.append(("sweep", self.rank, i, lo, cnt))
+
+
+class _LogExchanger:
+    def __init__(self, log, n_chunks):
+        self.log, self.n_chunks = log, n_chunks
+
+    def after_pre_chunk(self, t):
+        self.log.append(("pre", t))
+
+    def sync_point(self):
+        self.log.append(("sync",))
+
+    def launch_chunks(self, g_bits, p0, rx, factor):
+        self.log.append(("exchange",))
+
+    def wait_chunk(self, r, t):
+        self.log.append(("wait", r, t))
+
+
+@pytest.mark.parametrize("chunks", [2, 4, 8])
+def test_pipelined_schedule_covers_every_tile_once(chunks):
+    from paper_2312_03019_b200.sharded import _run_pipelined
+
+    nl, nt = 27, 1 << 15
+    # 3 local sets at n_local = 27: S0 (carry 12), S1 (carry 4, q 12), S2 (top: carry 5, q 20)
+    S0, S1, S2 = (12, 0), (4, 12), (5, 20)
+    segs = [[S1, S0], [S2, S2, S0], [S1, S1, S0], [S2]]   # exchange after each S0
+    plan = [(k, c, q, nt) for k, seg in enumerate(segs) for (c, q) in seg]
+    log = []
+    shards = [_PlanShard(plan, {0, 1, 2}, log, r) for r in range(2)]
+    relabels = []
+    _run_pipelined(shards, _LogExchanger(log, chunks), len(segs), 1, 11, nl,
+                   lambda: relabels.append(len(log)))
+    for r in range(2):
+        done = {}
+        for ev in log:
+            if ev[0] == "sweep" and ev[1] == r:
+                _, _, i, lo, cnt = ev
+                done.setdefault(i, []).append((lo, cnt))
+        assert sorted(done) == list(range(len(plan)))
+        for i, rs in done.items():
+            rs.sort()
+            assert rs[0][0] == 0 and sum(c for _, c in rs) == nt
+            assert all(a[0] + a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            if len(rs) > 1:  # only S0 (before an exchange) and non-top sweeps after one split
+                assert plan[i][1:3] in (S0, S1)
+    # one exchange per S0, each after all pre chunks and followed by the relabel
+    ex = [j for j, ev in enumerate(log) if ev == ("exchange",)]
+    assert len(ex) == 3 and len(relabels) == 3
+    for j, rl in zip(ex, relabels):
+        assert rl > j
+        pre = [ev[1] for ev in log[:j] if ev[0] == "pre"]
+        assert pre.count(chunks - 1) >= 1
