@@ -92,12 +92,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         }
       }
     }
-    const int64_t d = sk ? (int64_t)tile_off<C>(tile_index<2>(0, 1), Q) : 0;
-    const double2* se = amps + tc.base + tc.tb2 + d;
-    const double2* so = amps + tc.base + tc.tb2 - d;
-#pragma unroll
-    for (int r = 0; r < kRegs; ++r)
-      v[r] = __ldcs(((r & 1) ? so : se) + tile_off<C>(tile_index<2>(0, r), Q));
+    walk_tile<C, 2>(amps + tc.base + tc.tb2, Q, sk, [&](int r, double2* ptr) { v[r] = __ldcs(ptr); });
   }
   const bool need_cut = flags & (kPreCost | kMidCost | kExpect);
   if (need_cut) {
