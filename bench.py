@@ -230,6 +230,7 @@ def run_sharded(args, rank: int, world: int, local: int):
     import torch.distributed as tdist
 
     import paper_2312_03019_b200 as Q
+    from paper_2312_03019_b200 import _lib
     from paper_2312_03019_b200.sharded import (CudaShard, DistExchanger, IpcChunkExchanger,
                                                IpcExchanger, simulate_sharded,
                                                simulate_sharded_fused)
@@ -270,13 +271,23 @@ def run_sharded(args, rank: int, world: int, local: int):
     dist.barrier()
     torch.cuda.synchronize(local)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
     with ClockSampler(local) as clocks:
+        t0 = time.perf_counter()
         start.record()
         for _ in range(args.steps):
             val = step()
+            nl, hb = ctypes.c_int(), ctypes.c_double()
+            _lib.load().qaoa_last_run_stats(shard.eng.ptr, ctypes.byref(nl), ctypes.byref(hb))
+            launches += nl.value + (p * max(args.chunks, 1) if fused else 0)
         stop.record()
         torch.cuda.synchronize(local)
+        wall_s = time.perf_counter() - t0
     dev_ms = start.elapsed_time(stop)
+    tw = torch.tensor([wall_s], dtype=torch.float64,
+                      device="cpu" if args.dist_backend == "gloo" else f"cuda:{local}")
+    tdist.all_reduce(tw, op=tdist.ReduceOp.MAX)
+    wall_s = float(tw.item())
     t = torch.tensor([dev_ms], device="cpu" if args.dist_backend == "gloo" else f"cuda:{local}")
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     dev_ms = float(t.item())
@@ -291,8 +302,11 @@ def run_sharded(args, rank: int, world: int, local: int):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic",
             "config": {"workload": workload_name(args),
-                       "n_qubits": n, "p": p, "graph": args.graph, "parallelism": f"state sharded over {world} GPUs "
-                       f"(top {gbits} qubits), NCCL P2P exchange",
+                       "n_qubits": n, "p": p, "graph": args.graph,
+                       "parallelism": f"state sharded over {world} GPUs (top {gbits} qubits), "
+                       + (f"fused in-place exchange kernel over CUDA-IPC peer memory (NVLink P2P), "
+                          f"pipelined with the sweeps in {args.chunks} chunks"
+                          if fused else "NCCL P2P exchange + separate RX sweep"),
                        "l2": "no flush: shards >> L2"},
             "amp_updates_per_s": layers * per_level, "expectation": val,
             "test_mode": bool(args.share_device or args.dist_backend != "nccl"),
@@ -300,8 +314,14 @@ def run_sharded(args, rank: int, world: int, local: int):
                        "peak_GBps_per_direction": 770.0},
             "roofline": {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s",
                          "frac": None, "traffic": None, "peak_kind": peak_kind},
-            "cpu_baseline": None, "e2e": None,
-            "gpu_launches": None, "clocks": clocks.summary(),
+            "cpu_baseline": None,
+            # the sharded step is host-driven from host inputs (graph, angles ->
+            # phase tables and relabelled masks every level) to <C> on the host
+            "e2e": {"value": p * args.steps / wall_s, "unit": UNIT,
+                    "h2d_bytes_per_step": int(p * (16 * (g.tot_edge + 1) * 2 + 16) + 8 * n * (p + 1)),
+                    "d2h_bytes_per_step": 8,
+                    "api": "paper_2312_03019_b200.sharded.simulate_sharded_fused + sharded_expectation"},
+            "gpu_launches": launches, "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
     shard.close()

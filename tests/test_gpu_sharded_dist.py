@@ -34,3 +34,4 @@ def test_torchrun_sharded_bench(world, exchange, chunks):
     e = Q.expectation(g, Q.simulate(g, Q.params_from_seed(p, 0), "bitwise", max_qubits=n))
     assert line["expectation"] == pytest.approx(e, rel=1e-10)
     assert line["n_gpus"] == world and line["scaling"] == "strong" and line["test_mode"]
+    assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
