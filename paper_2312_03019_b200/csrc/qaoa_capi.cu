@@ -807,7 +807,6 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
   if (!c->has_graph) return fail(QAOA_E_STATE, "no graph set");
   if (p < 0) return fail(QAOA_E_INVALID, "level count must be non-negative");
   if (p > 0 && (!phase_tables || !cs || !sn)) return fail(QAOA_E_INVALID, "null angle arrays");
-  const bool exact = flags & QAOA_RUN_EXACT;
   const bool from_state = flags & QAOA_RUN_FROM_STATE;
   const bool want_expect = flags & QAOA_RUN_EXPECTATION;
   const bool timing = flags & QAOA_RUN_TIMING;

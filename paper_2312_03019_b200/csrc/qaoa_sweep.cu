@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     __syncthreads();
   }
   const int e = a.g.tot_edge;
-  const double r1a = a.rx1.a, r1b = a.rx1.b, r2a = a.rx2.a;
+  const double r1a = a.rx1.a, r1b = a.rx1.b;
   double acc = 0.0;
 
   if (FLOW == 0) {
@@ -128,70 +128,11 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     rx_regs2<A::g2, true>(v, r1a, r1b);
     if (flags & kExpect) acc = expect_acc<2>(v, &cb, tid, sk);
     store_tile<C, 2>(amps, tc, Q, v, flags, sk);
-  } else if (C >= 12) {
-    // ---- fast, low set: G2 (loaded), G0, G1 [, cost, G1, G0, G2]
-    if (flags & kPreCost) apply_cost<2>(v, &cb, a.table, e);
-    rx_regs2<A::g2, false>(v, r1a, 0.0);
-    exchange<2, 0>(buf, ts, v);
-    rx_regs2<A::g0, false>(v, r1a, 0.0);
-    exchange<0, 1>(buf, ts, v);
-    rx_regs2<A::g1, false>(v, r1a, 0.0);
-    if (FLOW == 2) {
-      apply_cost<1>(v, &cb, a.table2, e);
-      rx_regs2<A::g1, false>(v, r2a, 0.0);
-      exchange<1, 0>(buf, ts, v);
-      rx_regs2<A::g0, false>(v, r2a, 0.0);
-      exchange<0, 2>(buf, ts, v);
-      rx_regs2<A::g2, false>(v, r2a, 0.0);
-      if (flags & kScale) {
-#pragma unroll
-        for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
-      }
-      if (flags & kExpect) acc = expect_acc<2>(v, &cb);
-      store_tile<C, 2>(amps, tc, Q, v, flags);
-    } else {
-      if (flags & kScale) {
-#pragma unroll
-        for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
-      }
-      if (flags & kExpect) acc = expect_acc<1>(v, &cb);
-      store_tile<C, 1>(amps, tc, Q, v, flags);
-    }
   } else {
-    // ---- fast, high set: G2 (+ tile bit 3), G1 [, cost, G1 (+ tile bit 3), G2]
-    if (flags & kPreCost) apply_cost<2>(v, &cb, a.table, e, tid, sk);
-    rx_regs2<A::g2, false>(v, r1a, 0.0);
-    if (A::g0_shfl) {  // C = 3: tile bit 3 traded into register bit 0 (M2 -> M3)
-      transpose_lane3_sk(v);
-      rx_regs2<1u, false>(v, r1a, 0.0);
-      exchange<3, 1>(buf, ts, v, sk);
-      rx_regs2<A::g1, false>(v, r1a, 0.0);
-      if (FLOW == 2) {
-        apply_cost<1>(v, &cb, a.table2, e, tid, sk);
-        rx_regs2<A::g1, false>(v, r2a, 0.0);
-        transpose_lane3_sk(v);  // M1 -> M4
-        rx_regs2<1u, false>(v, r2a, 0.0);
-        exchange<4, 2>(buf, ts, v, sk);
-        rx_regs2<A::g2, false>(v, r2a, 0.0);
-      }
-    } else if (A::g1) {
-      exchange<2, 1>(buf, ts, v, sk);
-      rx_regs2<A::g1, false>(v, r1a, 0.0);
-      if (FLOW == 2) {
-        apply_cost<1>(v, &cb, a.table2, e, tid, sk);
-        rx_regs2<A::g1, false>(v, r2a, 0.0);
-        exchange<1, 2>(buf, ts, v, sk);
-        rx_regs2<A::g2, false>(v, r2a, 0.0);
-      }
-    } else if (FLOW == 2) {
-      apply_cost<2>(v, &cb, a.table2, e, tid, sk);
-      rx_regs2<A::g2, false>(v, r2a, 0.0);
-    }
-    constexpr int last = (A::g1 && FLOW == 1) ? 1 : 2;
-    if (flags & kScale) {
-#pragma unroll
-      for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
-    }
+    fast_tile<C, FLOW>(v, a, &cb, tid, sk, [&](auto from, auto to) {
+      exchange<decltype(from)::value, decltype(to)::value>(buf, ts, v, sk);
+    });
+    constexpr int last = fast_last<C, FLOW>();
     if (flags & kExpect) acc = expect_acc<last>(v, &cb, tid, sk);
     store_tile<C, last>(amps, tc, Q, v, flags, sk);
   }

@@ -202,8 +202,6 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
   }
   __syncthreads();
 
-  const int e = a.g.tot_edge;
-  const double r1a = a.rx1.a, r2a = a.rx2.a;
   unsigned long long* ctr = ta.counter;
   bool last = false;
   for (uint32_t j = 0;; ++j) {
@@ -264,73 +262,12 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
     tc.tb1 = tb1;
     double acc = 0.0;
 
-    if (C >= 12) {
-      // ---- low set: G2 (loaded), G0, G1 [, cost, G1, G0, G2]
-      if (flags & kPreCost) apply_cost<2>(v, cb, a.table, e, tid);
-      rx_regs2<A::g2, false>(v, r1a, 0.0);
-      exchange_bar<2, 0>(buf, ts, v, bar_id);
-      rx_regs2<A::g0, false>(v, r1a, 0.0);
-      exchange_bar<0, 1>(buf, ts, v, bar_id);
-      rx_regs2<A::g1, false>(v, r1a, 0.0);
-      if (FLOW == 2) {
-        apply_cost<1>(v, cb, a.table2, e, tid);
-        rx_regs2<A::g1, false>(v, r2a, 0.0);
-        exchange_bar<1, 0>(buf, ts, v, bar_id);
-        rx_regs2<A::g0, false>(v, r2a, 0.0);
-        exchange_bar<0, 2>(buf, ts, v, bar_id);
-        rx_regs2<A::g2, false>(v, r2a, 0.0);
-        if (flags & kScale) {
-#pragma unroll
-          for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
-        }
-        if (flags & kExpect) acc += expect_acc<2>(v, cb, tid);
-        finish_tile<C, 2, TS>(ta, tc, Q, v, buf, tid, bar_id, lo + tile, 0);
-      } else {
-        if (flags & kScale) {
-#pragma unroll
-          for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
-        }
-        if (flags & kExpect) acc += expect_acc<1>(v, cb, tid);
-        finish_tile<C, 1, TS>(ta, tc, Q, v, buf, tid, bar_id, lo + tile, 0);
-      }
-    } else {
-      // ---- high set: G2 (+ tile bit 3), G1 [, cost, G1 (+ tile bit 3), G2]
-      if (flags & kPreCost) apply_cost<2>(v, cb, a.table, e, tid, sk);
-      rx_regs2<A::g2, false>(v, r1a, 0.0);
-      if (A::g0_shfl) {
-        transpose_lane3_sk(v);
-        rx_regs2<1u, false>(v, r1a, 0.0);
-        exchange_bar<3, 1>(buf, ts, v, bar_id, sk);
-        rx_regs2<A::g1, false>(v, r1a, 0.0);
-        if (FLOW == 2) {
-          apply_cost<1>(v, cb, a.table2, e, tid, sk);
-          rx_regs2<A::g1, false>(v, r2a, 0.0);
-          transpose_lane3_sk(v);
-          rx_regs2<1u, false>(v, r2a, 0.0);
-          exchange_bar<4, 2>(buf, ts, v, bar_id, sk);
-          rx_regs2<A::g2, false>(v, r2a, 0.0);
-        }
-      } else if (A::g1) {
-        exchange_bar<2, 1>(buf, ts, v, bar_id, sk);
-        rx_regs2<A::g1, false>(v, r1a, 0.0);
-        if (FLOW == 2) {
-          apply_cost<1>(v, cb, a.table2, e, tid, sk);
-          rx_regs2<A::g1, false>(v, r2a, 0.0);
-          exchange_bar<1, 2>(buf, ts, v, bar_id, sk);
-          rx_regs2<A::g2, false>(v, r2a, 0.0);
-        }
-      } else if (FLOW == 2) {
-        apply_cost<2>(v, cb, a.table2, e, tid, sk);
-        rx_regs2<A::g2, false>(v, r2a, 0.0);
-      }
-      constexpr int last_m = (A::g1 && FLOW == 1) ? 1 : 2;
-      if (flags & kScale) {
-#pragma unroll
-        for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
-      }
-      if (flags & kExpect) acc += expect_acc<last_m>(v, cb, tid, sk);
-      finish_tile<C, last_m, TS>(ta, tc, Q, v, buf, tid, bar_id, lo + tile, sk);
-    }
+    fast_tile<C, FLOW>(v, a, cb, tid, sk, [&](auto from, auto to) {
+      exchange_bar<decltype(from)::value, decltype(to)::value>(buf, ts, v, bar_id, sk);
+    });
+    constexpr int last_m = fast_last<C, FLOW>();
+    if (flags & kExpect) acc += expect_acc<last_m>(v, cb, tid, sk);
+    finish_tile<C, last_m, TS>(ta, tc, Q, v, buf, tid, bar_id, lo + tile, sk);
     if (flags & kExpect) {
       // per-tile partial (fixed shuffle tree, warps in order): the sum over
       // tiles is then independent of which CTA ran which tile

@@ -5,6 +5,8 @@
 // the <C> accumulation.  Shared by qaoa_sweep.cu (one tile per CTA) and
 // qaoa_sweep_tma.cu (persistent, TMA-fed).
 #pragma once
+#include <type_traits>
+
 #include "qaoa_common.cuh"
 #include "qaoa_sweep.h"
 
@@ -187,7 +189,7 @@ __device__ __forceinline__ void half_coords(const SweepArgs& a, uint64_t tile, i
     if (C == 3) {
       c[1] = low; c[2] = 0; c[3] = h; c[4] = high;
     } else {
-      c[1] = 0; c[2] = low; c[3] = h << (11 - C); c[4] = high;
+      c[1] = 0; c[2] = low; c[3] = h << (C < 12 ? 11 - C : 0); c[4] = high;
     }
   }
 }
@@ -365,6 +367,77 @@ __device__ __forceinline__ void store_tile(double2* __restrict__ amps, const Til
   if (flags & kNoStore) return;
   const uint64_t tb = M == 2 ? tc.tb2 : tc.tb1;
   walk_tile<C, M>(amps + tc.base + tb, Q, sk, [&](int r, double2* ptr) { __stcs(ptr, v[r]); });
+}
+
+// ---- the register-tile work of a fast-schedule sweep ------------------------
+// Shared by both sweep kernels.  FLOW 1: [cost] RX(set); FLOW 2: [cost] RX(set)
+// -> cost -> RX(set) (two levels in one sweep).  `xchg(ic<A>, ic<B>)` re-maps
+// the registers from mapping A to B through the kernel's exchange buffer and
+// barrier.  The registers start in mapping M2 and end in fast_last<C, FLOW>().
+template <int V>
+using ic = std::integral_constant<int, V>;
+
+template <int C, int FLOW>
+__host__ __device__ constexpr int fast_last() {
+  return C >= 12 ? (FLOW == 2 ? 2 : 1) : ((Act<C>::g1 && FLOW == 1) ? 1 : 2);
+}
+
+template <int C, int FLOW, typename X>
+__device__ __forceinline__ void fast_tile(double2 (&v)[kRegs], const SweepArgs& a, const CutBasis* cb,
+                                          int tid, int sk, X&& xchg) {
+  using A = Act<C>;
+  const int e = a.g.tot_edge;
+  const double r1a = a.rx1.a, r2a = a.rx2.a;
+  if (a.flags & kPreCost) apply_cost<2>(v, cb, a.table, e, tid, sk);
+  if (C >= 12) {
+    // low set: G2 (loaded), G0, G1 [, cost, G1, G0, G2]
+    rx_regs2<A::g2, false>(v, r1a, 0.0);
+    xchg(ic<2>(), ic<0>());
+    rx_regs2<A::g0, false>(v, r1a, 0.0);
+    xchg(ic<0>(), ic<1>());
+    rx_regs2<A::g1, false>(v, r1a, 0.0);
+    if (FLOW == 2) {
+      apply_cost<1>(v, cb, a.table2, e, tid, sk);
+      rx_regs2<A::g1, false>(v, r2a, 0.0);
+      xchg(ic<1>(), ic<0>());
+      rx_regs2<A::g0, false>(v, r2a, 0.0);
+      xchg(ic<0>(), ic<2>());
+      rx_regs2<A::g2, false>(v, r2a, 0.0);
+    }
+  } else {
+    // high set: G2 (+ tile bit 3), G1 [, cost, G1 (+ tile bit 3), G2]
+    rx_regs2<A::g2, false>(v, r1a, 0.0);
+    if (A::g0_shfl) {  // C = 3: tile bit 3 traded into register bit 0 (M2 -> M3)
+      transpose_lane3_sk(v);
+      rx_regs2<1u, false>(v, r1a, 0.0);
+      xchg(ic<3>(), ic<1>());
+      rx_regs2<A::g1, false>(v, r1a, 0.0);
+      if (FLOW == 2) {
+        apply_cost<1>(v, cb, a.table2, e, tid, sk);
+        rx_regs2<A::g1, false>(v, r2a, 0.0);
+        transpose_lane3_sk(v);  // M1 -> M4
+        rx_regs2<1u, false>(v, r2a, 0.0);
+        xchg(ic<4>(), ic<2>());
+        rx_regs2<A::g2, false>(v, r2a, 0.0);
+      }
+    } else if (A::g1) {
+      xchg(ic<2>(), ic<1>());
+      rx_regs2<A::g1, false>(v, r1a, 0.0);
+      if (FLOW == 2) {
+        apply_cost<1>(v, cb, a.table2, e, tid, sk);
+        rx_regs2<A::g1, false>(v, r2a, 0.0);
+        xchg(ic<1>(), ic<2>());
+        rx_regs2<A::g2, false>(v, r2a, 0.0);
+      }
+    } else if (FLOW == 2) {
+      apply_cost<2>(v, cb, a.table2, e, tid, sk);
+      rx_regs2<A::g2, false>(v, r2a, 0.0);
+    }
+  }
+  if (a.flags & kScale) {
+#pragma unroll
+    for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], a.scale);
+  }
 }
 
 }  // namespace qb
