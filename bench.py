@@ -481,6 +481,11 @@ def run_ours(args, rank: int, world: int, local: int):
             "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
+        cl = line["clocks"]
+        if cl.get("power_w"):
+            # the sweeps run at the board power limit: energy per level is the
+            # figure that time follows
+            line["energy_j_per_level"] = cl["power_w"] * (dev_ms / args.steps) * 1e-3 / p
         print(json.dumps(line), flush=True)
     eng.close()
     if dist:
