@@ -190,6 +190,17 @@ QAOA_API int qaoa_synchronize(qaoa_ctx* ctx);
 QAOA_API int qaoa_pack_chunks(qaoa_ctx* ctx, int g, const int* local_bits, void* dst_device);
 QAOA_API int qaoa_unpack_chunks(qaoa_ctx* ctx, int g, const int* local_bits, const void* src_device);
 
+/* Weighted graphs, fast schedule: the same fused sweeps as qaoa_run_layers with
+ * the compressed backend's cost amp *= exp(-i gamma/2 sum_e w_e z_e(x))
+ * (cost.py:147-159) factored per tile (unit-modulus per-edge factors and a
+ * tile-internal table) instead of an integer phase table.  gammas[p]; c, s as
+ * in qaoa_run_layers; edges from qaoa_set_weights.  Within 1e-12 of the
+ * reference (not bit-identical: products instead of the edge-order sum);
+ * QAOA_RUN_EXACT / QAOA_RUN_SHARDED are refused, <C> via
+ * qaoa_expectation_weighted. */
+QAOA_API int qaoa_run_layers_weighted(qaoa_ctx* ctx, int p, const double* gammas, const double* c,
+                                      const double* s, int flags);
+
 /* ---- planned runs in segments (sharded states) -----------------------------
  * qaoa_run_layers = qaoa_run_begin + every qaoa_run_segment + qaoa_run_end.
  * With QAOA_RUN_SHARDED the plan stops after the low qubit set S_0 (local bits

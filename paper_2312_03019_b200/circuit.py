@@ -151,9 +151,10 @@ def simulate(
     ``device``, ``fuse_expectation`` (accumulate <C> in the last sweep) and
     ``state`` (reuse a StateVector's device buffer instead of allocating).
 
-    Weighted graphs (backends "compressed" / "baseline") run the compressed
-    weighted cost pass (cost.py:147-159) + the mixer sweeps per level: one more
-    HBM pass per level than the fused unweighted path."""
+    Weighted graphs (backends "compressed" / "baseline", cost.py:147-159): the
+    fast schedule runs the same fused sweeps with the weighted cost factored
+    per tile (within 1e-12 of the reference); ``exact=True`` (and n < 12) keeps
+    the reference's edge-order totals and the exact mixer, bit for bit."""
     validate_backend(backend, g)
     if batch_width is not None and batch_width not in (1, 2, 4, 8):
         raise ValueError(f"batch width must be 1, 2, 4, or 8, got {batch_width}")
@@ -167,12 +168,21 @@ def simulate(
         s = StateVector(g.n, engine=eng)
     eng.ensure_graph(g)
     if not g.is_unweighted:
-        eng.call("qaoa_init_uniform")
         eng.ensure_weights(g)
-        for gamma, beta in zip(params.gamma, params.beta):
-            eng.call("qaoa_apply_cost_weighted", float(gamma))
-            c, sn = rx_coefficients(beta)
-            eng.call("qaoa_apply_mixer", c, sn)
+        if not exact and g.n >= 12 and params.p > 0:
+            # fused sweeps with the factored weighted cost (within 1e-12)
+            gm = np.ascontiguousarray(np.array(params.gamma, dtype=np.float64))
+            cs = np.array([rx_coefficients(b)[0] for b in params.beta], dtype=np.float64)
+            ss = np.array([rx_coefficients(b)[1] for b in params.beta], dtype=np.float64)
+            eng.call("qaoa_run_layers_weighted", params.p, _lib.dptr(gm), _lib.dptr(cs),
+                     _lib.dptr(ss), 0)
+        else:
+            # reference order and rounding: edge-order totals, exact mixer sweeps
+            eng.call("qaoa_init_uniform")
+            for gamma, beta in zip(params.gamma, params.beta):
+                eng.call("qaoa_apply_cost_weighted", float(gamma))
+                c, sn = rx_coefficients(beta)
+                eng.call("qaoa_apply_mixer", c, sn)
         write_counter.add((1 << g.n) * (1 + params.p * (g.n + 1)))
         return s
     tables, cs, ss = level_arrays(g, params)

@@ -83,6 +83,7 @@ struct RunState {
   size_t ev = 0;
   int grid = 0;
   bool expect_fused = false;
+  bool weighted = false;  // factored weighted cost (qaoa_run_layers_weighted)
 };
 
 }  // namespace
@@ -117,6 +118,17 @@ struct qaoa_ctx {
   int* d_ej = nullptr;
   double* d_w = nullptr;
   int n_wedges = -1;
+  // factored weighted cost (fast schedule): host edge list, device endpoints,
+  // incidence lists, per-run u_e and tile-internal phase tables
+  std::vector<int> h_ei, h_ej;
+  std::vector<double> h_w;
+  int2* d_wedge = nullptr;
+  int* d_winc_off = nullptr;
+  int* d_winc = nullptr;
+  double2* d_wu = nullptr;
+  size_t d_wu_cap = 0;
+  double2* d_wq = nullptr;
+  size_t d_wq_cap = 0;
   // timing
   std::vector<cudaEvent_t> events;
   std::vector<float> times;
@@ -331,9 +343,10 @@ int create_common(int n, int device, void* stream, void* ext, qaoa_ctx** out) {
 // cmask covers the shard bits too), <C> is fused only when the run does not end
 // on an exchange.
 int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, const double* sn,
-              int flags, bool sharded) {
+              int flags, bool sharded, const double* gammas = nullptr) {
   RunState& R = c->run;
   R = RunState();
+  R.weighted = gammas != nullptr;
   R.exact = flags & QAOA_RUN_EXACT;
   R.from_state = flags & QAOA_RUN_FROM_STATE;
   R.want_expect = flags & QAOA_RUN_EXPECTATION;
@@ -363,13 +376,17 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
   R.level_factor.assign(std::max(p, 1), std::complex<double>(1.0, 0.0));
   std::complex<double> prev_scale(1.0, 0.0);
   if ((rc = ensure_tables(c, (size_t)te * std::max(p, 1)))) return rc;
+  std::vector<std::complex<double>> level_scale(std::max(p, 1));
   for (int l = 0; l < p; ++l) {
     const std::complex<double> f_scale = prev_scale;
-    const double* src = phase_tables + (size_t)2 * tl * l;
-    for (int k = 0; k < te; ++k) {
-      std::complex<double> v(src[4 * k], src[4 * k + 1]);
-      if (!R.exact) v *= f_scale;
-      c->h_tables[(size_t)l * te + k] = make_double2(v.real(), v.imag());
+    level_scale[l] = f_scale;
+    if (!R.weighted) {
+      const double* src = phase_tables + (size_t)2 * tl * l;
+      for (int k = 0; k < te; ++k) {
+        std::complex<double> v(src[4 * k], src[4 * k + 1]);
+        if (!R.exact) v *= f_scale;
+        c->h_tables[(size_t)l * te + k] = make_double2(v.real(), v.imag());
+      }
     }
     if (R.exact) {
       R.stages[l] = RxStage{cs[l], sn[l], 0};
@@ -387,10 +404,48 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
       R.flips ^= 1;
     }
   }
-  if (p > 0)
+  if (p > 0 && !R.weighted)
     CUDA_TRY(cudaMemcpyAsync(c->d_tables, c->h_tables, sizeof(double2) * (size_t)te * p,
                              cudaMemcpyHostToDevice, c->stream));
   R.final_scale = R.exact ? std::complex<double>(1.0, 0.0) : prev_scale;
+  if (R.weighted && p > 0) {
+    // u_e = exp(-i gamma_l w_e / 2) per level (cost.py:147-159), and the
+    // tile-internal phase table of the set where each level's cost is applied
+    const int m = c->n_wedges;
+    const size_t nu = (size_t)p * std::max(m, 1);
+    if (c->d_wu_cap < nu) {
+      if (c->d_wu) cudaFree(c->d_wu);
+      c->d_wu = nullptr;
+      c->d_wu_cap = 0;
+      CUDA_TRY(cudaMalloc(&c->d_wu, nu * sizeof(double2)));
+      c->d_wu_cap = nu;
+    }
+    const size_t nq = (size_t)p * 4096;
+    if (c->d_wq_cap < nq) {
+      if (c->d_wq) cudaFree(c->d_wq);
+      c->d_wq = nullptr;
+      c->d_wq_cap = 0;
+      CUDA_TRY(cudaMalloc(&c->d_wq, nq * sizeof(double2)));
+      c->d_wq_cap = nq;
+    }
+    std::vector<double2> hu(nu);
+    for (int l = 0; l < p; ++l)
+      for (int e = 0; e < m; ++e) {
+        const std::complex<double> u = std::exp(std::complex<double>(0.0, -0.5 * gammas[l] * c->h_w[e]));
+        hu[(size_t)l * m + e] = make_double2(u.real(), u.imag());
+      }
+    CUDA_TRY(cudaMemcpyAsync(c->d_wu, hu.data(), nu * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
+    for (int l = 0; l < p; ++l) {
+      int set = -1;
+      for (const SweepPlan& sp : R.plan)
+        if (sp.pre_cost == l || sp.mid_cost == l) set = sp.set;
+      const SetDesc& sd = R.sets[set < 0 ? 0 : set];
+      const std::complex<double> f = R.exact ? std::complex<double>(1.0, 0.0) : level_scale[l];
+      CUDA_TRY(launch_wq_table(c->d_wq + (size_t)l * 4096, c->d_wedge, c->d_wu + (size_t)l * m, m,
+                               sd.carry, sd.q, make_double2(f.real(), f.imag()), c->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));  // hu is a host temporary
+  }
 
   const int64_t ntiles = 1ll << (n - 12);
   R.grid = (int)ntiles;  // partials: one per tile
@@ -416,7 +471,7 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
   for (size_t i = 0; i < R.plan.size(); ++i)
     if (R.plan[i].exchange >= 0) R.seg_start.push_back((int)i + 1);
   if (R.seg_start.back() != (int)R.plan.size()) R.seg_start.push_back((int)R.plan.size());
-  R.expect_fused = R.want_expect && R.plan.back().exchange < 0;
+  R.expect_fused = R.want_expect && R.plan.back().exchange < 0 && !R.weighted;
   R.active = true;
   if ((rc = record_event(c, R.timing, R.ev++))) return rc;
   return QAOA_OK;
@@ -461,6 +516,22 @@ int launch_plan_sweep(qaoa_ctx* c, int i, int64_t lo, int64_t cnt) {
   if (sp.stage2 >= 0) {
     fl |= kStage2;
     a.rx2 = R.stages[sp.stage2];
+  }
+  if (R.weighted) {
+    const int m = c->n_wedges;
+    fl |= kWeighted;
+    a.wedge = c->d_wedge;
+    a.winc_off = c->d_winc_off;
+    a.winc = c->d_winc;
+    a.wm = m;
+    if (sp.pre_cost >= 0) {
+      a.wu1 = c->d_wu + (size_t)sp.pre_cost * m;
+      a.wq1 = c->d_wq + (size_t)sp.pre_cost * 4096;
+    }
+    if (sp.mid_cost >= 0) {
+      a.wu2 = c->d_wu + (size_t)sp.mid_cost * m;
+      a.wq2 = c->d_wq + (size_t)sp.mid_cost * 4096;
+    }
   }
   const bool last = i + 1 == (int)R.plan.size();
   if (last && !R.exact) {
@@ -556,6 +627,11 @@ void qaoa_destroy(qaoa_ctx* c) {
   if (c->d_ei) cudaFree(c->d_ei);
   if (c->d_ej) cudaFree(c->d_ej);
   if (c->d_w) cudaFree(c->d_w);
+  if (c->d_wedge) cudaFree(c->d_wedge);
+  if (c->d_winc_off) cudaFree(c->d_winc_off);
+  if (c->d_winc) cudaFree(c->d_winc);
+  if (c->d_wu) cudaFree(c->d_wu);
+  if (c->d_wq) cudaFree(c->d_wq);
   for (auto e : c->events) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -866,6 +942,23 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
   return run_end(c);
 }
 
+int qaoa_run_layers_weighted(qaoa_ctx* c, int p, const double* gammas, const double* cs,
+                             const double* sn, int flags) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (!c->has_graph) return fail(QAOA_E_STATE, "no graph set");
+  if (c->n_wedges < 0) return fail(QAOA_E_STATE, "no weights set (qaoa_set_weights)");
+  if (p < 1) return fail(QAOA_E_INVALID, "planned runs need at least one level");
+  if (!gammas || !cs || !sn) return fail(QAOA_E_INVALID, "null angle arrays");
+  if (c->n < 12) return fail(QAOA_E_INVALID, "the factored weighted schedule needs at least 12 qubits");
+  if (flags & (QAOA_RUN_EXACT | QAOA_RUN_SHARDED))
+    return fail(QAOA_E_INVALID, "the factored weighted schedule is fast-mode and unsharded only");
+  if ((rc = run_begin(c, p, nullptr, cs, sn, flags & ~QAOA_RUN_EXPECTATION, false, gammas))) return rc;
+  for (size_t k = 0; k + 1 < c->run.seg_start.size(); ++k)
+    if ((rc = run_segment(c, (int)k))) return rc;
+  return run_end(c);
+}
+
 int qaoa_run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs,
                    const double* sn, int flags, int* n_segments) {
   int rc = check_ctx(c);
@@ -1014,6 +1107,35 @@ int qaoa_set_weights(qaoa_ctx* c, int m, const int* ei, const int* ej, const dou
     CUDA_TRY(cudaMemcpyAsync(c->d_ej, ej, m * sizeof(int), cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->d_w, w, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   }
+  // endpoints + incidence lists for the factored cost of the fast schedule
+  c->h_ei.assign(ei, ei + m);
+  c->h_ej.assign(ej, ej + m);
+  c->h_w.assign(w, w + m);
+  std::vector<int2> edge(cnt, make_int2(0, 0));
+  std::vector<int> off(66, 0), inc(2 * cnt, 0);
+  for (int e = 0; e < m; ++e) {
+    edge[e] = make_int2(ei[e], ej[e]);
+    ++off[ei[e] + 1];
+    ++off[ej[e] + 1];
+  }
+  for (int i = 0; i < 65; ++i) off[i + 1] += off[i];
+  std::vector<int> fill(off.begin(), off.end() - 1);
+  for (int e = 0; e < m; ++e) {
+    inc[fill[ei[e]]++] = e;
+    inc[fill[ej[e]]++] = e;
+  }
+  if (c->d_wedge) cudaFree(c->d_wedge);
+  if (c->d_winc_off) cudaFree(c->d_winc_off);
+  if (c->d_winc) cudaFree(c->d_winc);
+  c->d_wedge = nullptr;
+  c->d_winc_off = nullptr;
+  c->d_winc = nullptr;
+  CUDA_TRY(cudaMalloc(&c->d_wedge, cnt * sizeof(int2)));
+  CUDA_TRY(cudaMalloc(&c->d_winc_off, 66 * sizeof(int)));
+  CUDA_TRY(cudaMalloc(&c->d_winc, 2 * cnt * sizeof(int)));
+  CUDA_TRY(cudaMemcpyAsync(c->d_wedge, edge.data(), cnt * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->d_winc_off, off.data(), 66 * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->d_winc, inc.data(), 2 * cnt * sizeof(int), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   c->n_wedges = m;
   c->expect_valid = false;

@@ -40,11 +40,13 @@ namespace qb {
 // FLOW 2: fast, RX stage -> cost -> RX stage (two levels in one sweep)
 // One 4096-amplitude tile per CTA; two CTAs per SM keep one tile's loads in
 // flight while the other computes (a persistent grid measured slower).
-template <bool WIDE, int C, int FLOW>
+// WGT: weighted cost (fast flows only; wbasis / apply_wcost in qaoa_tile.cuh).
+template <bool WIDE, int C, int FLOW, bool WGT = false>
 __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constant__ SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);  // kSlots exchange slots
   __shared__ CutBasis cb;
+  __shared__ WBasis wb[WGT ? 2 : 1];
   __shared__ double red_scratch[kThreads / 32];
   using A = Act<C>;
   // skewed register layout for the C = 3 flows (select-free transposes; the
@@ -96,7 +98,13 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   }
   const bool need_cut = flags & (kPreCost | kMidCost | kExpect);
   if (need_cut) {
-    if (tid < 32) cut_basis<WIDE, C>(a, tc.base, q, &cb);
+    if (tid < 32) {
+      if (WGT) {
+        if (flags & kPreCost) wbasis<C>(a, tc.base, q, a.wu1, &wb[0]);
+        if (flags & kMidCost) wbasis<C>(a, tc.base, q, a.wu2, &wb[WGT ? 1 : 0]);
+      }
+      if (!WGT || (flags & kExpect)) cut_basis<WIDE, C>(a, tc.base, q, &cb);
+    }
     __syncthreads();
   }
   const int e = a.g.tot_edge;
@@ -129,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     if (flags & kExpect) acc = expect_acc<2>(v, &cb, tid, sk);
     store_tile<C, 2>(amps, tc, Q, v, flags, sk);
   } else {
-    fast_tile<C, FLOW>(v, a, &cb, tid, sk, [&](auto from, auto to) {
+    fast_tile<C, FLOW, WGT>(v, a, &cb, wb, tid, sk, [&](auto from, auto to) {
       exchange<decltype(from)::value, decltype(to)::value>(buf, ts, v, sk);
     });
     constexpr int last = fast_last<C, FLOW>();
@@ -142,24 +150,57 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   }
 }
 
+// Tile-internal phase table of one weighted cost level (see apply_wcost).
+__global__ void wq_table_kernel(double2* __restrict__ out, const int2* __restrict__ wedge,
+                                const double2* __restrict__ wu, int wm, int carry, int q,
+                                double2 scale) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= kTile) return;
+  auto tile_bit = [&](int p) -> int {  // tile bit of physical node p, or -1
+    if (carry >= 12) return p < 12 ? p : -1;
+    if (p < carry) return p;
+    if (p >= q && p < q + 12 - carry) return carry + p - q;
+    return -1;
+  };
+  double2 f = scale;
+  for (int e = 0; e < wm; ++e) {
+    const int2 ij = wedge[e];
+    const int ki = tile_bit(ij.x), kj = tile_bit(ij.y);
+    if (ki < 0 || kj < 0) continue;
+    const double2 u = wu[e];
+    f = cmul_u(f, (((t >> ki) ^ (t >> kj)) & 1) ? conj2(u) : u);
+  }
+  out[t] = f;
+}
+
+cudaError_t launch_wq_table(double2* q_out, const int2* wedge, const double2* wu, int wm, int carry,
+                            int q, double2 scale, cudaStream_t s) {
+  wq_table_kernel<<<kTile / 256, 256, 0, s>>>(q_out, wedge, wu, wm, carry, q, scale);
+  return cudaGetLastError();
+}
+
 size_t sweep_smem_bytes(int) { return (size_t)kSlots * sizeof(double2); }
 
-template <bool WIDE, int C, int FLOW>
+template <bool WIDE, int C, int FLOW, bool WGT = false>
 static cudaError_t launch_one(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {
   static bool configured = false;  // per instantiation
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<WIDE, C, FLOW>,
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<WIDE, C, FLOW, WGT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  sweep_kernel<WIDE, C, FLOW><<<grid, kThreads, smem, s>>>(a);
+  sweep_kernel<WIDE, C, FLOW, WGT><<<grid, kThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 
 template <bool WIDE, int C>
 static cudaError_t launch_c(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {
   if (a.flags & kExact) return launch_one<WIDE, C, 0>(a, grid, smem, s);
+  if (a.flags & kWeighted) {
+    if (a.flags & kStage2) return launch_one<WIDE, C, 2, true>(a, grid, smem, s);
+    return launch_one<WIDE, C, 1, true>(a, grid, smem, s);
+  }
   if (a.flags & kStage2) return launch_one<WIDE, C, 2>(a, grid, smem, s);
   return launch_one<WIDE, C, 1>(a, grid, smem, s);
 }

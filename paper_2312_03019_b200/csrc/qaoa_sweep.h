@@ -18,6 +18,7 @@ enum SweepFlags : uint32_t {
   kScale = 1u << 6,    // multiply by `scale` before storing (fast mode)
   kExact = 1u << 7,    // reference arithmetic + increasing qubit order
   kNoStore = 1u << 8,  // read-only sweep
+  kWeighted = 1u << 9, // weighted cost: factored per-edge phases (see apply_wcost)
 };
 
 struct SweepArgs {
@@ -39,7 +40,23 @@ struct SweepArgs {
   uint32_t flags;
   int pf_dist;           // > 0: L2-prefetch tile (this tile + pf_dist) before loading this one
   int pf_tensor;         // prefetch through `map` (2 TMA prefetches) instead of per-run bulk prefetches
+  // weighted cost (kWeighted): u_e = exp(-i gamma w_e / 2) of the pre / mid
+  // level per edge, the 4096-entry tile-internal phase table of each, the edge
+  // endpoints (physical bits) and the per-node incidence lists (CSR)
+  const double2* wu1;
+  const double2* wu2;
+  const double2* wq1;
+  const double2* wq2;
+  const int2* wedge;
+  const int* winc_off;   // [65]
+  const int* winc;       // [2 wm] edge ids
+  int wm;
 };
+// Tile-internal phase table of one weighted cost level for tile geometry (C, q):
+// Q[t] = scale * prod over edges with both endpoints tile nodes of u_e (equal
+// true bits) or conj(u_e) (different), t = true tile index.
+cudaError_t launch_wq_table(double2* q_out, const int2* wedge, const double2* wu, int wm, int carry,
+                            int q, double2 scale, cudaStream_t s);
 // 5-D tensor map of the state for tile geometry (C, q) (qaoa_sweep_tma.cu).
 bool make_tile_map(CUtensorMap* map, void* amps, int n, int C, int q);
 

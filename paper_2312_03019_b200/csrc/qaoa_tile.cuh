@@ -287,6 +287,107 @@ __device__ __forceinline__ void cut16(const CutBasis* cb, int (&c)[16], int tid,
   c[15] = c[7] + d[3] - a03 - a13 - a23;
 }
 
+// ---- weighted cost, factored (fast schedule) --------------------------------
+// amp *= exp(-i gamma/2 sum_e w_e z_e(x)), z_e = +1 when the endpoints agree, -1
+// when cut (reference cost.py:147-159, compressed backend).  With the non-tile
+// bits h of a tile fixed, the phase factors into
+//   F(h) * prod_{tile nodes k} (x_k ? conj(B_k) : B_k) * Q[t]
+// F = edges outside the tile, B_k = edges from tile node k to outside (for
+// x_k = 0), Q = edges inside the tile (a per-geometry table of the true tile
+// index, built once per level).  All factors have unit modulus, so flipping a
+// register bit multiplies by conj(B)^2 or B^2.  ~16 FP64 ops per amplitude
+// instead of an edge-order sum plus sincos per amplitude; not bit-identical to
+// the reference's sum (~1e-15 relative), the exact schedule keeps that path.
+struct WBasis {
+  double2 F;
+  double2 B[12];
+  int tmask;
+};
+
+__device__ __forceinline__ double2 cmul_u(double2 a, double2 b) {
+  return make_double2(__fma_rn(a.x, b.x, -a.y * b.y), __fma_rn(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 conj2(double2 a) { return make_double2(a.x, -a.y); }
+
+// Warp-wide basis of one tile (call from one full warp).
+template <int C>
+__device__ __forceinline__ void wbasis(const SweepArgs& a, uint64_t base, int q, const double2* __restrict__ wu,
+                                       WBasis* wb) {
+  const uint64_t tile_phys = (C >= 12) ? 0xFFFull
+                                       : (((1ull << C) - 1ull) | (((1ull << (12 - C)) - 1ull) << q));
+  const uint64_t h = (a.g.x_hi ^ a.g.cmask ^ base) & ~tile_phys;
+  const int lane = threadIdx.x & 31;
+  double2 f = make_double2(1.0, 0.0);
+  for (int e = lane; e < a.wm; e += 32) {
+    const int2 ij = __ldg(a.wedge + e);
+    if (((tile_phys >> ij.x) & 1ull) | ((tile_phys >> ij.y) & 1ull)) continue;
+    const double2 u = __ldg(wu + e);
+    f = cmul_u(f, (((h >> ij.x) ^ (h >> ij.y)) & 1ull) ? conj2(u) : u);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double2 other;
+    other.x = __shfl_xor_sync(0xffffffffu, f.x, o);
+    other.y = __shfl_xor_sync(0xffffffffu, f.y, o);
+    f = cmul_u(f, other);
+  }
+  if (lane < 12) {
+    const int p = tile_pos<C>(lane, q);
+    double2 b = make_double2(1.0, 0.0);
+    for (int idx = __ldg(a.winc_off + p); idx < __ldg(a.winc_off + p + 1); ++idx) {
+      const int e = __ldg(a.winc + idx);
+      const int2 ij = __ldg(a.wedge + e);
+      const int j = ij.x == p ? ij.y : ij.x;
+      if ((tile_phys >> j) & 1ull) continue;
+      const double2 u = __ldg(wu + e);
+      b = cmul_u(b, ((h >> j) & 1ull) ? conj2(u) : u);
+    }
+    wb->B[lane] = b;
+  }
+  if (lane == 0) {
+    const uint64_t cm = a.g.cmask;
+    wb->F = f;
+    wb->tmask = (int)((C >= 12) ? (cm & 0xFFFull)
+                                : ((cm & ((1ull << C) - 1ull)) |
+                                   (((cm >> q) & ((1ull << (12 - C)) - 1ull)) << C)));
+  }
+}
+
+// Registers of mapping M (M2 or M1) times the weighted phase of their basis
+// states; register combinations visited in Gray-code order (one complex
+// multiply per register for the running B product).
+template <int M>
+__device__ __forceinline__ void apply_wcost(double2 (&v)[kRegs], const WBasis* wb,
+                                            const double2* __restrict__ qt, int tid, int sk) {
+  constexpr int g = group_of<M>();
+  const int T = tile_index<M>(tid, 0) ^ wb->tmask ^ (sk ? tile_index<M>(0, 1) : 0);
+  double2 cur = wb->F;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    const double2 b = wb->B[k];
+    cur = cmul_u(cur, ((T >> k) & 1) ? conj2(b) : b);
+  }
+  double2 up[4];  // multiplier when register bit j flips away from T's value
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double2 b = wb->B[4 * g + j];
+    const double2 b2 = cmul_u(b, b);
+    up[j] = ((T >> (4 * g + j)) & 1) ? b2 : conj2(b2);
+  }
+  int prev = 0;
+#pragma unroll
+  for (int k = 0; k < kRegs; ++k) {
+    const int r = k ^ (k >> 1);  // Gray order
+    if (k) {
+      const int j = (r ^ prev) == 1 ? 0 : (r ^ prev) == 2 ? 1 : (r ^ prev) == 4 ? 2 : 3;
+      cur = cmul_u(cur, (r >> j) & 1 ? up[j] : conj2(up[j]));
+    }
+    prev = r;
+    const double2 ph = cmul_u(cur, __ldg(qt + ((T ^ tile_index<M>(0, r)) & 0xFFF)));
+    v[r] = cmul_u(v[r], ph);
+  }
+}
+
 // amp *= table_even[E - C(x)] (table_even[k] = phase_table[2k]; reference
 // cost.py:168-172 indexes table[(E - 2C) + E]).
 template <int M>
@@ -382,13 +483,17 @@ __host__ __device__ constexpr int fast_last() {
   return C >= 12 ? (FLOW == 2 ? 2 : 1) : ((Act<C>::g1 && FLOW == 1) ? 1 : 2);
 }
 
-template <int C, int FLOW, typename X>
+// WGT: weighted cost (apply_wcost with wb[0] / wb[1] for the pre / mid level).
+template <int C, int FLOW, bool WGT = false, typename X>
 __device__ __forceinline__ void fast_tile(double2 (&v)[kRegs], const SweepArgs& a, const CutBasis* cb,
-                                          int tid, int sk, X&& xchg) {
+                                          const WBasis* wb, int tid, int sk, X&& xchg) {
   using A = Act<C>;
   const int e = a.g.tot_edge;
   const double r1a = a.rx1.a, r2a = a.rx2.a;
-  if (a.flags & kPreCost) apply_cost<2>(v, cb, a.table, e, tid, sk);
+  if (a.flags & kPreCost) {
+    if (WGT) apply_wcost<2>(v, &wb[0], a.wq1, tid, sk);
+    else apply_cost<2>(v, cb, a.table, e, tid, sk);
+  }
   if (C >= 12) {
     // low set: G2 (loaded), G0, G1 [, cost, G1, G0, G2]
     rx_regs2<A::g2, false>(v, r1a, 0.0);
@@ -397,7 +502,8 @@ __device__ __forceinline__ void fast_tile(double2 (&v)[kRegs], const SweepArgs& 
     xchg(ic<0>(), ic<1>());
     rx_regs2<A::g1, false>(v, r1a, 0.0);
     if (FLOW == 2) {
-      apply_cost<1>(v, cb, a.table2, e, tid, sk);
+      if (WGT) apply_wcost<1>(v, &wb[1], a.wq2, tid, sk);
+      else apply_cost<1>(v, cb, a.table2, e, tid, sk);
       rx_regs2<A::g1, false>(v, r2a, 0.0);
       xchg(ic<1>(), ic<0>());
       rx_regs2<A::g0, false>(v, r2a, 0.0);
@@ -413,7 +519,8 @@ __device__ __forceinline__ void fast_tile(double2 (&v)[kRegs], const SweepArgs& 
       xchg(ic<3>(), ic<1>());
       rx_regs2<A::g1, false>(v, r1a, 0.0);
       if (FLOW == 2) {
-        apply_cost<1>(v, cb, a.table2, e, tid, sk);
+        if (WGT) apply_wcost<1>(v, &wb[1], a.wq2, tid, sk);
+        else apply_cost<1>(v, cb, a.table2, e, tid, sk);
         rx_regs2<A::g1, false>(v, r2a, 0.0);
         transpose_lane3_sk(v);  // M1 -> M4
         rx_regs2<1u, false>(v, r2a, 0.0);
@@ -424,13 +531,15 @@ __device__ __forceinline__ void fast_tile(double2 (&v)[kRegs], const SweepArgs& 
       xchg(ic<2>(), ic<1>());
       rx_regs2<A::g1, false>(v, r1a, 0.0);
       if (FLOW == 2) {
-        apply_cost<1>(v, cb, a.table2, e, tid, sk);
+        if (WGT) apply_wcost<1>(v, &wb[1], a.wq2, tid, sk);
+        else apply_cost<1>(v, cb, a.table2, e, tid, sk);
         rx_regs2<A::g1, false>(v, r2a, 0.0);
         xchg(ic<1>(), ic<2>());
         rx_regs2<A::g2, false>(v, r2a, 0.0);
       }
     } else if (FLOW == 2) {
-      apply_cost<2>(v, cb, a.table2, e, tid, sk);
+      if (WGT) apply_wcost<2>(v, &wb[1], a.wq2, tid, sk);
+      else apply_cost<2>(v, cb, a.table2, e, tid, sk);
       rx_regs2<A::g2, false>(v, r2a, 0.0);
     }
   }

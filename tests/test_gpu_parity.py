@@ -299,3 +299,25 @@ def test_weighted_larger_against_unweighted_limit():
         Q.apply_mixer_layer(s, bt)
     assert np.max(np.abs(s.amps - a.amps)) <= AMP_TOL
     assert eng.scalar("qaoa_expectation_weighted") == pytest.approx(Q.expectation(g, a), rel=1e-12)
+
+
+@pytest.mark.parametrize("n,dense", [(12, False), (13, True), (16, False), (20, False), (21, True),
+                                     (22, False), (26, False), (25, True)])
+def test_weighted_fused_fast_matches_exact(n, dense):
+    """The fast schedule's factored weighted cost (fused sweeps) against the
+    reference-order weighted path (edge-order totals, bit-identical to the
+    reference): amplitudes <= 1e-12, <C> <= 1e-10 relative, including levels
+    that take the second RX form (complement bookkeeping)."""
+    rng = np.random.default_rng(n)
+    base = Q.erdos_renyi_graph(n, 0.5, seed=n) if dense else Q.random_regular_graph(n, 3, seed=n)
+    g = Q.Graph.from_edges(n, [(i, j, float(rng.uniform(0.1, 2.0))) for i, j, _ in base.edges])
+    assert not g.is_unweighted
+    for betas in ((0.4, 1.1), (2.9, 0.3, 3.05)):
+        gammas = tuple(0.3 + 0.8 * k for k in range(len(betas)))
+        pr = Q.QaoaParams(gammas, betas)
+        ref = Q.simulate(g, pr, "compressed", max_qubits=30, exact=True)
+        ref_amps = ref.amps
+        e_ref = Q.expectation(g, ref)
+        f = Q.simulate(g, pr, "compressed", max_qubits=30)
+        assert np.max(np.abs(f.amps - ref_amps)) <= AMP_TOL, (n, betas)
+        assert Q.expectation(g, f) == pytest.approx(e_ref, rel=EXP_RTOL)
