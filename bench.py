@@ -248,11 +248,26 @@ def run_sharded(args, rank: int, world: int, local: int):
     fused = args.exchange == "ipc"
     shard = CudaShard(n - gbits, rank, device=local, exact=args.exact,
                       stream=None if fused else torch.cuda.current_stream(local).cuda_stream)
-    if fused and args.chunks > 1:
-        exch = IpcChunkExchanger(shard, rank, world, args.chunks)
-    elif fused:
-        exch = IpcExchanger(shard, rank, world)
-    else:
+    fallback = None
+    exch = None
+    if fused:
+        try:
+            exch = (IpcChunkExchanger(shard, rank, world, args.chunks) if args.chunks > 1
+                    else IpcExchanger(shard, rank, world))
+        except Exception as exc:  # no CUDA IPC / peer access between these GPUs
+            fallback = f"CUDA IPC unavailable ({exc}); NCCL staging path used"
+    ok = torch.tensor([0 if (fused and exch is None) else 1], dtype=torch.int32,
+                      device="cpu" if args.dist_backend == "gloo" else f"cuda:{local}")
+    tdist.all_reduce(ok, op=tdist.ReduceOp.MIN)
+    if fused and int(ok.item()) == 0:  # every rank must take the same path
+        if exch is not None and hasattr(exch, "close"):
+            exch.close()
+        fused, exch = False, None
+        fallback = fallback or "a peer could not map CUDA IPC; NCCL staging path used"
+        shard.close()
+        shard = CudaShard(n - gbits, rank, device=local, exact=args.exact,
+                          stream=torch.cuda.current_stream(local).cuda_stream)
+    if exch is None:
         exch = DistExchanger(shard, rank, world)
 
     def step():
@@ -310,6 +325,7 @@ def run_sharded(args, rank: int, world: int, local: int):
                        "l2": "no flush: shards >> L2"},
             "amp_updates_per_s": layers * per_level, "expectation": val,
             "test_mode": bool(args.share_device or args.dist_backend != "nccl"),
+            "exchange_fallback": fallback,
             "nvlink": {"bytes_per_level_per_rank_per_direction": xbytes,
                        "peak_GBps_per_direction": 770.0},
             "roofline": {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s",
