@@ -43,6 +43,9 @@ extern "C" {
 #define QAOA_RUN_EXPECTATION 0x4    /* fuse <C> into the last sweep (qaoa_expectation)  */
 #define QAOA_RUN_TIMING 0x8         /* record per-launch CUDA-event times               */
 #define QAOA_RUN_SHARDED 0x10       /* qaoa_run_begin: exchange points after S_0 of every level */
+#define QAOA_RUN_EXPECT_ONLY 0x20   /* with QAOA_RUN_EXPECTATION: the last sweep only reads (16 B
+                                       instead of 32 B per amplitude); the state is left unusable
+                                       (amplitude reads and QAOA_RUN_FROM_STATE then fail) */
 
 typedef struct qaoa_ctx qaoa_ctx;
 

@@ -31,6 +31,7 @@ RUN_FROM_STATE = 0x2
 RUN_EXPECTATION = 0x4
 RUN_TIMING = 0x8
 RUN_SHARDED = 0x10
+RUN_EXPECT_ONLY = 0x20
 
 _c_int = ctypes.c_int
 _c_dbl = ctypes.c_double

@@ -142,6 +142,7 @@ def simulate(
     device: int = 0,
     fuse_expectation: bool = True,
     state: StateVector | None = None,
+    store_state: bool = True,
 ) -> StateVector:
     """Run the p-level circuit on the GPU and return the device-resident state
     (circuit.py:97-113).  All three backend names select the fused engine (they
@@ -149,7 +150,10 @@ def simulate(
 
     Extra keyword-only knobs: ``exact`` (bit-exact reference schedule),
     ``device``, ``fuse_expectation`` (accumulate <C> in the last sweep) and
-    ``state`` (reuse a StateVector's device buffer instead of allocating).
+    ``state`` (reuse a StateVector's device buffer instead of allocating) and
+    ``store_state=False`` (only <C> is wanted: the last sweep reads without
+    writing back, and the returned state may only be passed to
+    ``expectation`` or reused as ``state=``; the optimizer uses it).
 
     Weighted graphs (backends "compressed" / "baseline", cost.py:147-159): the
     fast schedule runs the same fused sweeps with the weighted cost factored
@@ -187,6 +191,8 @@ def simulate(
         return s
     tables, cs, ss = level_arrays(g, params)
     flags = (_lib.RUN_EXACT if exact else 0) | (_lib.RUN_EXPECTATION if fuse_expectation else 0)
+    if not store_state and fuse_expectation:
+        flags |= _lib.RUN_EXPECT_ONLY
     eng.call("qaoa_run_layers", params.p, _lib.dptr(tables.view(np.float64)), _lib.dptr(cs),
              _lib.dptr(ss), flags)
     write_counter.add((1 << g.n) * (1 + params.p * (g.n + 1)))

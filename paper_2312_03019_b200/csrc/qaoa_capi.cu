@@ -84,6 +84,7 @@ struct RunState {
   int grid = 0;
   bool expect_fused = false;
   bool weighted = false;  // factored weighted cost (qaoa_run_layers_weighted)
+  bool no_store_last = false;  // QAOA_RUN_EXPECT_ONLY
 };
 
 }  // namespace
@@ -135,6 +136,7 @@ struct qaoa_ctx {
   int last_launches = 0;
   double last_bytes = 0.0;
   RunState run;
+  bool state_stale = false;  // last run skipped its final store (QAOA_RUN_EXPECT_ONLY)
 };
 
 namespace {
@@ -145,6 +147,13 @@ int check_ctx(qaoa_ctx* c) {
   if (!c) return fail(QAOA_E_INVALID, "null context");
   cudaError_t e = cudaSetDevice(c->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  return QAOA_OK;
+}
+
+// A state left unstored by a QAOA_RUN_EXPECT_ONLY run must not be read.
+int require_stored(qaoa_ctx* c) {
+  if (c->state_stale)
+    return fail(QAOA_E_STATE, "the state was not stored by the last run (QAOA_RUN_EXPECT_ONLY)");
   return QAOA_OK;
 }
 
@@ -362,6 +371,8 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
   c->last_bytes = 0.0;
   c->times.clear();
   int rc;
+  if (R.from_state && c->state_stale)
+    return fail(QAOA_E_STATE, "the state was not stored by the last run (QAOA_RUN_EXPECT_ONLY)");
   if (!R.from_state) c->g.cmask = 0;
 
   R.sets = make_sets(n);
@@ -472,6 +483,7 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
     if (R.plan[i].exchange >= 0) R.seg_start.push_back((int)i + 1);
   if (R.seg_start.back() != (int)R.plan.size()) R.seg_start.push_back((int)R.plan.size());
   R.expect_fused = R.want_expect && R.plan.back().exchange < 0 && !R.weighted;
+  R.no_store_last = (flags & QAOA_RUN_EXPECT_ONLY) && R.expect_fused;
   R.active = true;
   if ((rc = record_event(c, R.timing, R.ev++))) return rc;
   return QAOA_OK;
@@ -539,6 +551,7 @@ int launch_plan_sweep(qaoa_ctx* c, int i, int64_t lo, int64_t cnt) {
     a.scale = make_double2(R.final_scale.real(), R.final_scale.imag());
   }
   if (last && R.expect_fused) fl |= kExpect;
+  if (last && R.no_store_last) fl |= kNoStore;
   a.flags = fl;
   CUDA_TRY(launch_sweep(a, R.grid, c->stream));
   ++c->last_launches;
@@ -563,6 +576,7 @@ int run_end(qaoa_ctx* c) {
   RunState& R = c->run;
   if (!R.active) return fail(QAOA_E_STATE, "no planned run (qaoa_run_begin)");
   R.active = false;
+  c->state_stale = R.no_store_last;
   int rc;
   if (R.flips) {
     // sharded: complement all n_nodes bits (C(x) = C(~x) keeps the cost kernels
@@ -682,6 +696,7 @@ int qaoa_set_graph(qaoa_ctx* c, int n_nodes, const uint64_t* row_mask, int tot_e
 int qaoa_init_uniform(qaoa_ctx* c) {
   int rc = check_ctx(c);
   if (rc) return rc;
+  c->state_stale = false;
   const int n_total = c->has_graph ? c->g.n_nodes : c->n;
   const double u = sqrt(1.0 / (double)(1ull << n_total));
   CUDA_TRY(launch_fill(c->amps, 1ull << c->n, make_double2(u, 0.0), c->stream));
@@ -702,6 +717,9 @@ static void permute_chunk(double2* dst, const double2* src, uint64_t true_off, u
 int qaoa_write_amplitudes(qaoa_ctx* c, uint64_t offset, uint64_t count, const double* src) {
   int rc = check_ctx(c);
   if (rc) return rc;
+  if (c->state_stale && !(offset == 0 && count == (1ull << c->n)))
+    return fail(QAOA_E_STATE, "the state was not stored by the last run (QAOA_RUN_EXPECT_ONLY)");
+  c->state_stale = false;
   const uint64_t size = 1ull << c->n;
   if (offset + count > size || offset + count < offset)
     return fail(QAOA_E_RANGE, "amplitude range out of bounds");
@@ -736,6 +754,8 @@ int qaoa_write_amplitudes(qaoa_ctx* c, uint64_t offset, uint64_t count, const do
 int qaoa_read_amplitudes(qaoa_ctx* c, uint64_t offset, uint64_t count, double* dst) {
   int rc = check_ctx(c);
   if (rc) return rc;
+  if (c->state_stale)
+    return fail(QAOA_E_STATE, "the state was not stored by the last run (QAOA_RUN_EXPECT_ONLY)");
   const uint64_t size = 1ull << c->n;
   if (offset + count > size || offset + count < offset)
     return fail(QAOA_E_RANGE, "amplitude range out of bounds");
@@ -773,6 +793,7 @@ int qaoa_set_cmask(qaoa_ctx* c, uint64_t cmask) {
 int qaoa_apply_cost(qaoa_ctx* c, const double* phase_table) {
   int rc = check_ctx(c);
   if (rc) return rc;
+  if ((rc = require_stored(c))) return rc;
   if (!c->has_graph) return fail(QAOA_E_STATE, "no graph set");
   if (!phase_table) return fail(QAOA_E_INVALID, "null phase table");
   const size_t len = 2 * (size_t)c->g.tot_edge + 1;
@@ -789,6 +810,7 @@ int qaoa_apply_cost(qaoa_ctx* c, const double* phase_table) {
 int qaoa_apply_rx(qaoa_ctx* c, int qubit, double cs, double sn) {
   int rc = check_ctx(c);
   if (rc) return rc;
+  if ((rc = require_stored(c))) return rc;
   if (qubit < 0 || qubit >= c->n) {
     char buf[96];
     snprintf(buf, sizeof buf, "qubit %d out of range for n=%d", qubit, c->n);
@@ -823,6 +845,7 @@ static int run_exact_mixer_sweeps(qaoa_ctx* c, double cs, double sn) {
 int qaoa_apply_mixer(qaoa_ctx* c, double cs, double sn) {
   int rc = check_ctx(c);
   if (rc) return rc;
+  if ((rc = require_stored(c))) return rc;
   if (c->n >= 12) {
     if ((rc = run_exact_mixer_sweeps(c, cs, sn))) return rc;
   } else {
@@ -836,6 +859,7 @@ int qaoa_apply_mixer(qaoa_ctx* c, double cs, double sn) {
 int qaoa_apply_rx_range(qaoa_ctx* c, int q0, int count, double cs, double sn, int flags) {
   int rc = check_ctx(c);
   if (rc) return rc;
+  if ((rc = require_stored(c))) return rc;
   if (count < 1 || q0 < 0 || q0 + count > c->n)
     return fail(QAOA_E_RANGE, "qubit range out of bounds");
   const bool exact = flags & QAOA_RUN_EXACT;
@@ -899,6 +923,9 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
 
   if (n < 12) {
     // Small states: per-gate kernels (bit-exact in both modes).
+    if (from_state && c->state_stale)
+      return fail(QAOA_E_STATE, "the state was not stored by the last run (QAOA_RUN_EXPECT_ONLY)");
+    c->state_stale = false;
     if ((rc = ensure_tables(c, (size_t)tl * std::max(p, 1)))) return rc;
     memcpy(c->h_tables, phase_tables, sizeof(double2) * (size_t)tl * p);
     CUDA_TRY(cudaMemcpyAsync(c->d_tables, c->h_tables, sizeof(double2) * (size_t)tl * p,
@@ -1145,6 +1172,7 @@ int qaoa_set_weights(qaoa_ctx* c, int m, const int* ei, const int* ej, const dou
 int qaoa_apply_cost_weighted(qaoa_ctx* c, double gamma) {
   int rc = check_ctx(c);
   if (rc) return rc;
+  if ((rc = require_stored(c))) return rc;
   if (c->n_wedges < 0) return fail(QAOA_E_STATE, "no weighted edge list set");
   const uint64_t xbase = c->g.x_hi ^ c->g.cmask;
   CUDA_TRY(launch_cost_weighted(c->amps, 1ull << c->n, xbase, c->d_ei, c->d_ej, c->d_w,
@@ -1170,6 +1198,7 @@ int qaoa_expectation_weighted(qaoa_ctx* c, double* out) {
 int qaoa_block_norms(qaoa_ctx* c, int block_bits, double* out) {
   int rc = check_ctx(c);
   if (rc) return rc;
+  if ((rc = require_stored(c))) return rc;
   if (block_bits < 0 || block_bits > 12 || block_bits > c->n || !out)
     return fail(QAOA_E_INVALID, "bad block size");
   const uint64_t nb = 1ull << (c->n - block_bits);
@@ -1224,6 +1253,7 @@ int qaoa_expectation(qaoa_ctx* c, double* out) {
     *out = c->expect_value;
     return QAOA_OK;
   }
+  if ((rc = require_stored(c))) return rc;
   const int grid = reduce_grid();
   if ((rc = ensure_partials(c, grid))) return rc;
   CUDA_TRY(launch_expectation(c->amps, c->n, c->g, c->partials, grid, c->stream));
@@ -1236,6 +1266,7 @@ int qaoa_expectation(qaoa_ctx* c, double* out) {
 int qaoa_norm_sq(qaoa_ctx* c, double* out) {
   int rc = check_ctx(c);
   if (rc) return rc;
+  if ((rc = require_stored(c))) return rc;
   if (!out) return fail(QAOA_E_INVALID, "null output");
   const int grid = reduce_grid();
   if ((rc = ensure_partials(c, grid))) return rc;
@@ -1335,6 +1366,7 @@ int qaoa_synchronize(qaoa_ctx* c) {
 int qaoa_pack_chunks(qaoa_ctx* c, int g, const int* local_bits, void* dst) {
   int rc = check_ctx(c);
   if (rc) return rc;
+  if ((rc = require_stored(c))) return rc;
   if (g < 0 || g > 8 || g > c->n || (g && (!local_bits || !dst)))
     return fail(QAOA_E_INVALID, "bad chunk spec");
   for (int k = 0; k < g; ++k) {

@@ -133,3 +133,20 @@ def test_brute_force_uses_gpu_cut_table():
     g = Q.random_regular_graph(16, 3, seed=4)
     cut = Q.brute_force_max_cut(g)
     assert cut.value == max(Q.cut_value(g, b) for b in range(0, 1 << 16, 1))
+
+
+def test_expectation_only_run():
+    """store_state=False: the last sweep only reads; <C> is the stored run's, the
+    state refuses amplitude reads and is reusable as a buffer (the optimizer's
+    inner loop)."""
+    g = Q.random_regular_graph(20, 3, seed=3)
+    pr = Q.params_from_seed(3, 1)
+    full = Q.simulate(g, pr, "bitwise")
+    e_full = Q.expectation(g, full)
+    for exact in (False, True):
+        s = Q.simulate(g, pr, "bitwise", store_state=False, exact=exact)
+        assert Q.expectation(g, s) == pytest.approx(e_full, rel=1e-10)
+        with pytest.raises(Exception, match="not stored"):
+            _ = s.amps
+        s2 = Q.simulate(g, pr, "bitwise", state=s, exact=exact)
+        assert np.max(np.abs(s2.amps - full.amps)) <= 1e-12
