@@ -199,8 +199,9 @@ QAOA_API int qaoa_unpack_chunks(qaoa_ctx* ctx, int g, const int* local_bits, con
  * tile-internal table) instead of an integer phase table.  gammas[p]; c, s as
  * in qaoa_run_layers; edges from qaoa_set_weights.  Within 1e-12 of the
  * reference (not bit-identical: products instead of the edge-order sum);
- * QAOA_RUN_EXACT / QAOA_RUN_SHARDED are refused, <C> via
- * qaoa_expectation_weighted. */
+ * QAOA_RUN_EXACT / QAOA_RUN_SHARDED are refused.  QAOA_RUN_EXPECTATION fuses
+ * the weighted <C> (graph.py:144-151, read by qaoa_expectation_weighted) into
+ * the last sweep. */
 QAOA_API int qaoa_run_layers_weighted(qaoa_ctx* ctx, int p, const double* gammas, const double* c,
                                       const double* s, int flags);
 

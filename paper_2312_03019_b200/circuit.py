@@ -178,8 +178,11 @@ def simulate(
             gm = np.ascontiguousarray(np.array(params.gamma, dtype=np.float64))
             cs = np.array([rx_coefficients(b)[0] for b in params.beta], dtype=np.float64)
             ss = np.array([rx_coefficients(b)[1] for b in params.beta], dtype=np.float64)
+            wflags = _lib.RUN_EXPECTATION if fuse_expectation else 0
+            if not store_state and fuse_expectation:
+                wflags |= _lib.RUN_EXPECT_ONLY
             eng.call("qaoa_run_layers_weighted", params.p, _lib.dptr(gm), _lib.dptr(cs),
-                     _lib.dptr(ss), 0)
+                     _lib.dptr(ss), wflags)
         else:
             # reference order and rounding: edge-order totals, exact mixer sweeps
             eng.call("qaoa_init_uniform")

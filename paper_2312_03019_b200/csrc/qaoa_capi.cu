@@ -113,6 +113,7 @@ struct qaoa_ctx {
   // true index).  Bits >= n are the shard bits (managed by the sharded host).
   // expectation cached from the last fused run
   bool expect_valid = false;
+  bool expect_is_weighted = false;  // the cached value is the weighted cut's
   double expect_value = 0.0;
   // weighted edge list (compressed backend), device copies
   int* d_ei = nullptr;
@@ -130,6 +131,7 @@ struct qaoa_ctx {
   size_t d_wu_cap = 0;
   double2* d_wq = nullptr;
   size_t d_wq_cap = 0;
+  double* d_wc = nullptr;  // tile-internal cut weights of the last sweep's set (fused weighted <C>)
   // timing
   std::vector<cudaEvent_t> events;
   std::vector<float> times;
@@ -434,6 +436,7 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
     const size_t nq = (size_t)p * 4096;
     if (c->d_wq_cap < nq) {
       if (c->d_wq) cudaFree(c->d_wq);
+  if (c->d_wc) cudaFree(c->d_wc);
       c->d_wq = nullptr;
       c->d_wq_cap = 0;
       CUDA_TRY(cudaMalloc(&c->d_wq, nq * sizeof(double2)));
@@ -482,7 +485,12 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
   for (size_t i = 0; i < R.plan.size(); ++i)
     if (R.plan[i].exchange >= 0) R.seg_start.push_back((int)i + 1);
   if (R.seg_start.back() != (int)R.plan.size()) R.seg_start.push_back((int)R.plan.size());
-  R.expect_fused = R.want_expect && R.plan.back().exchange < 0 && !R.weighted;
+  R.expect_fused = R.want_expect && R.plan.back().exchange < 0;
+  if (R.expect_fused && R.weighted) {
+    if (!c->d_wc) CUDA_TRY(cudaMalloc(&c->d_wc, 4096 * sizeof(double)));
+    const SetDesc& sd = R.sets[R.plan.back().set];
+    CUDA_TRY(launch_wc_table(c->d_wc, c->d_wedge, c->d_w, c->n_wedges, sd.carry, sd.q, c->stream));
+  }
   R.no_store_last = (flags & QAOA_RUN_EXPECT_ONLY) && R.expect_fused;
   R.active = true;
   if ((rc = record_event(c, R.timing, R.ev++))) return rc;
@@ -536,6 +544,8 @@ int launch_plan_sweep(qaoa_ctx* c, int i, int64_t lo, int64_t cnt) {
     a.winc_off = c->d_winc_off;
     a.winc = c->d_winc;
     a.wm = m;
+    a.ww = c->d_w;
+    a.wc = c->d_wc;
     if (sp.pre_cost >= 0) {
       a.wu1 = c->d_wu + (size_t)sp.pre_cost * m;
       a.wq1 = c->d_wq + (size_t)sp.pre_cost * 4096;
@@ -589,6 +599,7 @@ int run_end(qaoa_ctx* c) {
     if ((rc = reduce_to_host(c, R.grid, 0, &c->expect_value))) return rc;
     ++c->last_launches;
     c->expect_valid = true;
+    c->expect_is_weighted = R.weighted;
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   if (R.timing) {
@@ -980,7 +991,7 @@ int qaoa_run_layers_weighted(qaoa_ctx* c, int p, const double* gammas, const dou
   if (c->n < 12) return fail(QAOA_E_INVALID, "the factored weighted schedule needs at least 12 qubits");
   if (flags & (QAOA_RUN_EXACT | QAOA_RUN_SHARDED))
     return fail(QAOA_E_INVALID, "the factored weighted schedule is fast-mode and unsharded only");
-  if ((rc = run_begin(c, p, nullptr, cs, sn, flags & ~QAOA_RUN_EXPECTATION, false, gammas))) return rc;
+  if ((rc = run_begin(c, p, nullptr, cs, sn, flags, false, gammas))) return rc;
   for (size_t k = 0; k + 1 < c->run.seg_start.size(); ++k)
     if ((rc = run_segment(c, (int)k))) return rc;
   return run_end(c);
@@ -1187,6 +1198,11 @@ int qaoa_expectation_weighted(qaoa_ctx* c, double* out) {
   if (rc) return rc;
   if (!out) return fail(QAOA_E_INVALID, "null output");
   if (c->n_wedges < 0) return fail(QAOA_E_STATE, "no weighted edge list set");
+  if (c->expect_valid && c->expect_is_weighted) {  // fused into the last weighted run
+    *out = c->expect_value;
+    return QAOA_OK;
+  }
+  if ((rc = require_stored(c))) return rc;
   const int grid = reduce_grid();
   if ((rc = ensure_partials(c, grid))) return rc;
   const uint64_t xbase = c->g.x_hi ^ c->g.cmask;
@@ -1249,7 +1265,7 @@ int qaoa_expectation(qaoa_ctx* c, double* out) {
   if (rc) return rc;
   if (!out) return fail(QAOA_E_INVALID, "null output");
   if (!c->has_graph) return fail(QAOA_E_STATE, "no graph set");
-  if (c->expect_valid) {
+  if (c->expect_valid && !c->expect_is_weighted) {
     *out = c->expect_value;
     return QAOA_OK;
   }

@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   double2* buf = reinterpret_cast<double2*>(smem_raw);  // kSlots exchange slots
   __shared__ CutBasis cb;
   __shared__ WBasis wb[WGT ? 2 : 1];
+  __shared__ WCutBasis wcb[1];
   __shared__ double red_scratch[kThreads / 32];
   using A = Act<C>;
   // skewed register layout for the C = 3 flows (select-free transposes; the
@@ -103,7 +104,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         if (flags & kPreCost) wbasis<C>(a, tc.base, q, a.wu1, &wb[0]);
         if (flags & kMidCost) wbasis<C>(a, tc.base, q, a.wu2, &wb[WGT ? 1 : 0]);
       }
-      if (!WGT || (flags & kExpect)) cut_basis<WIDE, C>(a, tc.base, q, &cb);
+      if (WGT && (flags & kExpect)) wcut_basis<C>(a, tc.base, q, &wcb[0]);
+      if (!WGT) cut_basis<WIDE, C>(a, tc.base, q, &cb);
     }
     __syncthreads();
   }
@@ -141,7 +143,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
       exchange<decltype(from)::value, decltype(to)::value>(buf, ts, v, sk);
     });
     constexpr int last = fast_last<C, FLOW>();
-    if (flags & kExpect) acc = expect_acc<last>(v, &cb, tid, sk);
+    if (flags & kExpect)
+      acc = WGT ? expect_wacc<last>(v, &wcb[0], a.wc, tid, sk) : expect_acc<last>(v, &cb, tid, sk);
     store_tile<C, last>(amps, tc, Q, v, flags, sk);
   }
   if (flags & kExpect) {
@@ -176,6 +179,32 @@ __global__ void wq_table_kernel(double2* __restrict__ out, const int2* __restric
 cudaError_t launch_wq_table(double2* q_out, const int2* wedge, const double2* wu, int wm, int carry,
                             int q, double2 scale, cudaStream_t s) {
   wq_table_kernel<<<kTile / 256, 256, 0, s>>>(q_out, wedge, wu, wm, carry, q, scale);
+  return cudaGetLastError();
+}
+
+__global__ void wc_table_kernel(double* __restrict__ out, const int2* __restrict__ wedge,
+                                const double* __restrict__ w, int wm, int carry, int q) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= kTile) return;
+  auto tile_bit = [&](int p) -> int {
+    if (carry >= 12) return p < 12 ? p : -1;
+    if (p < carry) return p;
+    if (p >= q && p < q + 12 - carry) return carry + p - q;
+    return -1;
+  };
+  double c = 0.0;
+  for (int e = 0; e < wm; ++e) {
+    const int2 ij = wedge[e];
+    const int ki = tile_bit(ij.x), kj = tile_bit(ij.y);
+    if (ki < 0 || kj < 0) continue;
+    if (((t >> ki) ^ (t >> kj)) & 1) c += w[e];
+  }
+  out[t] = c;
+}
+
+cudaError_t launch_wc_table(double* c_out, const int2* wedge, const double* w, int wm, int carry, int q,
+                            cudaStream_t s) {
+  wc_table_kernel<<<kTile / 256, 256, 0, s>>>(c_out, wedge, w, wm, carry, q);
   return cudaGetLastError();
 }
 

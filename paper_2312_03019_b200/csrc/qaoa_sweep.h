@@ -51,12 +51,18 @@ struct SweepArgs {
   const int* winc_off;   // [65]
   const int* winc;       // [2 wm] edge ids
   int wm;
+  const double* ww;      // [wm] edge weights (weighted <C>)
+  const double* wc;      // 4096-entry tile-internal cut weight table of the last sweep's set
 };
 // Tile-internal phase table of one weighted cost level for tile geometry (C, q):
 // Q[t] = scale * prod over edges with both endpoints tile nodes of u_e (equal
 // true bits) or conj(u_e) (different), t = true tile index.
 cudaError_t launch_wq_table(double2* q_out, const int2* wedge, const double2* wu, int wm, int carry,
                             int q, double2 scale, cudaStream_t s);
+// Tile-internal weighted cut table: C[t] = sum of w_e over cut edges with both
+// endpoints tile nodes (true tile index t), for the fused weighted <C>.
+cudaError_t launch_wc_table(double* c_out, const int2* wedge, const double* w, int wm, int carry, int q,
+                            cudaStream_t s);
 // 5-D tensor map of the state for tile geometry (C, q) (qaoa_sweep_tma.cu).
 bool make_tile_map(CUtensorMap* map, void* amps, int n, int C, int q);
 

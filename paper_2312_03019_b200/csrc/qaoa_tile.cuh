@@ -353,6 +353,81 @@ __device__ __forceinline__ void wbasis(const SweepArgs& a, uint64_t base, int q,
   }
 }
 
+// Weighted cut value of the tile's basis states (fused weighted <C>, graph.py
+// 144-151 up to summation order): cut_w(h|t) = hh + sum_k (x_k ? W_k - S_k : S_k)
+// + Cint[t], S_k = weight from tile node k to set non-tile nodes, W_k = all its
+// weight to non-tile nodes, Cint = edges inside the tile.
+struct WCutBasis {
+  double hh;
+  double S[12];
+  double W[12];
+  int tmask;
+};
+
+template <int C>
+__device__ __forceinline__ void wcut_basis(const SweepArgs& a, uint64_t base, int q, WCutBasis* wb) {
+  const uint64_t tile_phys = (C >= 12) ? 0xFFFull
+                                       : (((1ull << C) - 1ull) | (((1ull << (12 - C)) - 1ull) << q));
+  const uint64_t h = (a.g.x_hi ^ a.g.cmask ^ base) & ~tile_phys;
+  const int lane = threadIdx.x & 31;
+  double hh = 0.0;
+  for (int e = lane; e < a.wm; e += 32) {
+    const int2 ij = __ldg(a.wedge + e);
+    if (((tile_phys >> ij.x) & 1ull) | ((tile_phys >> ij.y) & 1ull)) continue;
+    if (((h >> ij.x) ^ (h >> ij.y)) & 1ull) hh += __ldg(a.ww + e);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) hh += __shfl_xor_sync(0xffffffffu, hh, o);
+  if (lane < 12) {
+    const int p = tile_pos<C>(lane, q);
+    double S = 0.0, W = 0.0;
+    for (int idx = __ldg(a.winc_off + p); idx < __ldg(a.winc_off + p + 1); ++idx) {
+      const int e = __ldg(a.winc + idx);
+      const int2 ij = __ldg(a.wedge + e);
+      const int j = ij.x == p ? ij.y : ij.x;
+      if ((tile_phys >> j) & 1ull) continue;
+      const double w = __ldg(a.ww + e);
+      W += w;
+      if ((h >> j) & 1ull) S += w;
+    }
+    wb->S[lane] = S;
+    wb->W[lane] = W;
+  }
+  if (lane == 0) {
+    const uint64_t cm = a.g.cmask;
+    wb->hh = hh;
+    wb->tmask = (int)((C >= 12) ? (cm & 0xFFFull)
+                                : ((cm & ((1ull << C) - 1ull)) |
+                                   (((cm >> q) & ((1ull << (12 - C)) - 1ull)) << C)));
+  }
+}
+
+template <int M>
+__device__ __forceinline__ double expect_wacc(const double2 (&v)[kRegs], const WCutBasis* wb,
+                                              const double* __restrict__ cint, int tid, int sk) {
+  constexpr int g = group_of<M>();
+  const int T = tile_index<M>(tid, 0) ^ wb->tmask ^ (sk ? tile_index<M>(0, 1) : 0);
+  double base = wb->hh;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) base += ((T >> k) & 1) ? wb->W[k] - wb->S[k] : wb->S[k];
+  double d[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double S = wb->S[4 * g + j], W = wb->W[4 * g + j];
+    d[j] = ((T >> (4 * g + j)) & 1) ? 2.0 * S - W : W - 2.0 * S;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    double val = base + __ldg(cint + ((T ^ tile_index<M>(0, r)) & 0xFFF));
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if ((r >> j) & 1) val += d[j];
+    acc += (v[r].x * v[r].x + v[r].y * v[r].y) * val;
+  }
+  return acc;
+}
+
 // Registers of mapping M (M2 or M1) times the weighted phase of their basis
 // states; register combinations visited in Gray-code order (one complex
 // multiply per register for the running B product).

@@ -319,5 +319,8 @@ def test_weighted_fused_fast_matches_exact(n, dense):
         ref_amps = ref.amps
         e_ref = Q.expectation(g, ref)
         f = Q.simulate(g, pr, "compressed", max_qubits=30)
+        e_f = Q.expectation(g, f)  # fused into the last sweep
         assert np.max(np.abs(f.amps - ref_amps)) <= AMP_TOL, (n, betas)
-        assert Q.expectation(g, f) == pytest.approx(e_ref, rel=EXP_RTOL)
+        assert e_f == pytest.approx(e_ref, rel=EXP_RTOL)
+        o = Q.simulate(g, pr, "compressed", max_qubits=30, store_state=False)
+        assert Q.expectation(g, o) == pytest.approx(e_ref, rel=EXP_RTOL)
