@@ -213,11 +213,15 @@ def run_reference(args, rank: int, world: int):
 def make_graph(Q, args):
     if args.graph == "er":
         return Q.erdos_renyi_graph(args.n, 0.5, seed=0)
+    if args.n % 2:  # no 3-regular graph on an odd node count: u3r(N-1) plus an isolated node
+        base = Q.random_regular_graph(args.n - 1, 3, seed=0)
+        return Q.Graph.from_edges(args.n, list(base.edges))
     return Q.random_regular_graph(args.n, 3, seed=0)
 
 
 def workload_name(args) -> str:
-    gname = "u3r" if args.graph == "u3r" else "ER(0.5)"
+    gname = ("u3r" if args.n % 2 == 0 else f"u3r({args.n - 1}) + isolated node") \
+        if args.graph == "u3r" else "ER(0.5)"
     cfg = {("u3r", 30, 10): "BASELINE configs[2]", ("er", 33, 4): "BASELINE configs[3]",
            ("u3r", 26, 4): "BASELINE configs[1]", ("u3r", 20, 1): "BASELINE configs[0]"}
     tag = cfg.get((args.graph, args.n, args.p), "custom")
