@@ -618,7 +618,7 @@ extern "C" {
 
 const char* qaoa_last_error(void) { return g_last_error.c_str(); }
 
-const char* qaoa_version(void) { return "qaoa_b200 0.1 sm_100a"; }
+const char* qaoa_version(void) { return "qaoa_b200 0.2 sm_100a"; }
 
 int qaoa_device_count(void) {
   int n = 0;
