@@ -523,18 +523,26 @@ class IpcChunkExchanger(IpcExchanger):
     host barriers per exchange (over a gloo group: no device synchronisation)
     order the event records before the waits."""
 
-    def __init__(self, shard: CudaShard, rank: int, world: int, n_chunks: int, group=None):
+    def __init__(self, shard: CudaShard, rank: int, world: int, n_chunks: int, group=None,
+                 ipc_events: bool | None = None):
+        import os
+
         import torch
         import torch.distributed as dist
 
         super().__init__(shard, rank, world, group)
         self.n_chunks = n_chunks
         self.cpu_group = dist.new_group(backend="gloo")
+        if ipc_events is None:  # QAOA_IPC_EVENTS=0: host barriers per chunk instead
+            ipc_events = os.environ.get("QAOA_IPC_EVENTS", "1") != "0"
+        self.ipc_events = ipc_events
         dev = shard.device
         self.xstream = torch.cuda.Stream(dev, priority=-1)
-        mk = lambda: torch.cuda.Event(interprocess=True, enable_timing=False)  # noqa: E731
+        mk = lambda: torch.cuda.Event(interprocess=ipc_events, enable_timing=False)  # noqa: E731
         self.my_pre = [mk() for _ in range(n_chunks)]
         self.my_x = [mk() for _ in range(n_chunks)]
+        if not ipc_events:
+            return
         # events must exist on the device before their IPC handles are taken
         with torch.cuda.stream(shard.stream):
             for e in self.my_pre + self.my_x:
@@ -551,26 +559,38 @@ class IpcChunkExchanger(IpcExchanger):
     def after_pre_chunk(self, t: int) -> None:
         self.my_pre[t].record(self.shard.stream)
 
-    def sync_point(self) -> None:
+    def _host_barrier(self) -> None:
         import torch.distributed as dist
 
         dist.barrier(group=self.cpu_group)
+
+    def sync_point(self) -> None:
+        if self.ipc_events:
+            self._host_barrier()
 
     def launch_chunks(self, g_bits, p0, rx, factor) -> None:
         sh = self.shard
         cols = 1 << (sh.n - g_bits)
         c, G, r = self.n_chunks, self.world, self.rank
         for t in range(c):
-            for rr in range(G):
-                self.xstream.wait_event(self.pre[rr][t])
+            if self.ipc_events:
+                for rr in range(G):
+                    self.xstream.wait_event(self.pre[rr][t])
+            else:  # every rank's chunk t of the sweep is done
+                self.my_pre[t].synchronize()
+                self._host_barrier()
             lo, hi = cols * t // c, cols * (t + 1) // c
             _exchange_call(sh.device, self.xstream.cuda_stream, g_bits, self.ptrs, sh.n, p0,
                            lo + (hi - lo) * r // G, lo + (hi - lo) * (r + 1) // G, rx, factor)
             self.my_x[t].record(self.xstream)
 
     def wait_chunk(self, shard_index: int, t: int) -> None:
-        for rr in range(self.world):
-            self.shard.stream.wait_event(self.x[rr][t])
+        if self.ipc_events:
+            for rr in range(self.world):
+                self.shard.stream.wait_event(self.x[rr][t])
+        else:  # every rank's exchange chunk t landed
+            self.my_x[t].synchronize()
+            self._host_barrier()
 
 
 def simulate_sharded_fused(g: Graph, params: QaoaParams, shards: Sequence[CudaShard], exchanger,

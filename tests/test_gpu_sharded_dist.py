@@ -16,18 +16,20 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("world,exchange,chunks", [(2, "ipc", 4), (4, "ipc", 4), (4, "ipc", 1),
-                                                   (2, "nccl", 1), (4, "nccl", 1)])
-def test_torchrun_sharded_bench(world, exchange, chunks):
+@pytest.mark.parametrize("world,exchange,chunks,events", [(2, "ipc", 4, 1), (4, "ipc", 4, 1),
+                                                          (4, "ipc", 4, 0), (4, "ipc", 1, 1),
+                                                          (2, "nccl", 1, 1), (4, "nccl", 1, 1)])
+def test_torchrun_sharded_bench(world, exchange, chunks, events):
     """ipc: the fused exchange kernel with the peers' shards mapped by CUDA IPC
     (here all on one device); nccl: the staging path."""
     n, p = 22, 3
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + (10 if exchange == "ipc" else 0) + chunks),
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + (10 if exchange == "ipc" else 0) + chunks + 20 * events),
            os.path.join(ROOT, "bench.py"), "--gpus", str(world), "--steps", "2", "--warmup", "3",
            "--qubits", str(n), "--levels", str(p), "--dist-backend", "gloo", "--share-device",
            "--exchange", exchange, "--chunks", str(chunks)]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    env = dict(os.environ, QAOA_IPC_EVENTS=str(events))
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     g = Q.random_regular_graph(n, 3, seed=0)
