@@ -205,6 +205,13 @@ QAOA_API int qaoa_unpack_chunks(qaoa_ctx* ctx, int g, const int* local_bits, con
 QAOA_API int qaoa_run_layers_weighted(qaoa_ctx* ctx, int p, const double* gammas, const double* c,
                                       const double* s, int flags);
 
+/* The sweep plan of qaoa_run_layers / qaoa_run_begin for n_local qubits and p
+ * levels (flags: QAOA_RUN_EXACT, QAOA_RUN_SHARDED), without a device: writes up
+ * to `cap` sweeps as 7 ints each (carry, q, pre-cost level, stage-1 level,
+ * mid-cost level, stage-2 level, exchange level; -1 = none) and returns the
+ * sweep count (or a negative status). */
+QAOA_API int qaoa_plan(int n_local, int p, int flags, int* out, int cap);
+
 /* ---- planned runs in segments (sharded states) -----------------------------
  * qaoa_run_layers = qaoa_run_begin + every qaoa_run_segment + qaoa_run_end.
  * With QAOA_RUN_SHARDED the plan stops after the low qubit set S_0 (local bits

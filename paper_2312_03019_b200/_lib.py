@@ -81,6 +81,7 @@ SIGNATURES = {
     "qaoa_pack_chunks": (_c_int, [_vp, _c_int, _ip, _vp]),
     "qaoa_unpack_chunks": (_c_int, [_vp, _c_int, _ip, _vp]),
     "qaoa_run_layers_weighted": (_c_int, [_vp, _c_int, _dp, _dp, _dp, _c_int]),
+    "qaoa_plan": (_c_int, [_c_int, _c_int, _c_int, _ip, _c_int]),
     "qaoa_run_begin": (_c_int, [_vp, _c_int, _dp, _dp, _dp, _c_int, _ip]),
     "qaoa_run_segment": (_c_int, [_vp, _c_int]),
     "qaoa_run_exchange_info": (_c_int, [_vp, _c_int, _ip, _dp, _dp]),

@@ -980,6 +980,28 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
   return run_end(c);
 }
 
+int qaoa_plan(int n_local, int p, int flags, int* out, int cap) {
+  if (n_local < 12 || n_local > 40 || p < 1) return fail(QAOA_E_INVALID, "plan needs n_local in [12, 40], p >= 1");
+  const std::vector<SetDesc> sets = make_sets(n_local);
+  const std::vector<SweepPlan> plan =
+      make_plan((int)sets.size(), p, (flags & QAOA_RUN_EXACT) != 0, (flags & QAOA_RUN_SHARDED) != 0);
+  if (out) {
+    for (size_t i = 0; i < plan.size() && (int)i < cap; ++i) {
+      const SweepPlan& sp = plan[i];
+      const SetDesc& sd = sets[sp.set];
+      int* o = out + 7 * i;
+      o[0] = sd.carry;
+      o[1] = sd.q;
+      o[2] = sp.pre_cost;
+      o[3] = sp.stage1;
+      o[4] = sp.mid_cost;
+      o[5] = sp.stage2;
+      o[6] = sp.exchange;
+    }
+  }
+  return (int)plan.size();
+}
+
 int qaoa_run_layers_weighted(qaoa_ctx* c, int p, const double* gammas, const double* cs,
                              const double* sn, int flags) {
   int rc = check_ctx(c);
