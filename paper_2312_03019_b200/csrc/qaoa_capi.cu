@@ -937,31 +937,26 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
     if (from_state && c->state_stale)
       return fail(QAOA_E_STATE, "the state was not stored by the last run (QAOA_RUN_EXPECT_ONLY)");
     c->state_stale = false;
-    if ((rc = ensure_tables(c, (size_t)tl * std::max(p, 1)))) return rc;
-    memcpy(c->h_tables, phase_tables, sizeof(double2) * (size_t)tl * p);
-    CUDA_TRY(cudaMemcpyAsync(c->d_tables, c->h_tables, sizeof(double2) * (size_t)tl * p,
+    // one CTA runs the whole circuit with the state in shared memory
+    // (small_run_kernel): phase tables then the per-level (c, s) pairs
+    const size_t nt = (size_t)tl * p;
+    if ((rc = ensure_tables(c, nt + std::max(p, 1)))) return rc;
+    memcpy(c->h_tables, phase_tables, sizeof(double2) * nt);
+    for (int l = 0; l < p; ++l) c->h_tables[nt + l] = make_double2(cs[l], sn[l]);
+    CUDA_TRY(cudaMemcpyAsync(c->d_tables, c->h_tables, sizeof(double2) * (nt + p),
                              cudaMemcpyHostToDevice, c->stream));
+    if (!from_state) c->g.cmask = 0;
     if ((rc = record_event(c, timing, ev++))) return rc;
-    if (!from_state) {
-      CUDA_TRY(launch_fill(c->amps, size, make_double2(u, 0.0), c->stream));
-      ++c->last_launches;
-      c->g.cmask = 0;
-    }
-    for (int l = 0; l < p; ++l) {
-      CUDA_TRY(launch_cost_gate(c->amps, size, c->g, c->d_tables + (size_t)l * tl, c->stream));
-      ++c->last_launches;
-      for (int q = 0; q < n; ++q) {
-        CUDA_TRY(launch_rx_gate(c->amps, n, q, cs[l], sn[l], c->stream));
-        ++c->last_launches;
-      }
-    }
+    CUDA_TRY(launch_small_run(c->amps, n, c->g, c->d_tables, c->d_tables + nt, p, from_state ? 1 : 0, u,
+                              want_expect ? 1 : 0, c->d_scalar, c->stream));
+    ++c->last_launches;
+    c->last_bytes += 16.0 * size * (from_state ? 2 : 1);
     if ((rc = record_event(c, timing, ev++))) return rc;
     if (want_expect) {
-      const int grid = reduce_grid();
-      CUDA_TRY(launch_expectation(c->amps, n, c->g, c->partials, grid, c->stream));
-      ++c->last_launches;
-      if ((rc = reduce_to_host(c, grid, 0, &c->expect_value))) return rc;
+      CUDA_TRY(cudaMemcpyAsync(&c->expect_value, c->d_scalar, sizeof(double), cudaMemcpyDeviceToHost,
+                               c->stream));
       c->expect_valid = true;
+      c->expect_is_weighted = false;
     }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (timing) {

@@ -113,6 +113,69 @@ cudaError_t launch_rx_gate(double2* amps, int n_local, int q, double c, double s
   return cudaGetLastError();
 }
 
+// ---- whole circuit for small states (n <= 11) in ONE CTA -------------------
+// The state (<= 2048 amplitudes, 32 KB) lives in shared memory for all p
+// levels: launch control, per level the cost (cost.py:162-176, FMA-form
+// multiply) and RX on every qubit in increasing order (state.py:110-128, the
+// reference's rounding), then <C> (fixed-order block sum).  The same
+// operations in the same order as the per-gate kernels, so bit-identical to
+// them and to the reference; one launch instead of p (n + 1) + 2.
+template <bool WIDE>
+__global__ void __launch_bounds__(kBlock) small_run_kernel(double2* __restrict__ amps, int n, GraphDev g,
+                                                           const double2* __restrict__ tables,
+                                                           const double2* __restrict__ rx, int p,
+                                                           int from_state, double u, int want_expect,
+                                                           double* __restrict__ expect_out) {
+  extern __shared__ double2 st[];
+  __shared__ double scratch[kBlock / 32];
+  const int N = 1 << n;
+  const int tl = 2 * g.tot_edge + 1;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) st[i] = from_state ? amps[i] : make_double2(u, 0.0);
+  __syncthreads();
+  for (int l = 0; l < p; ++l) {
+    const double2* tab = tables + (size_t)l * tl;
+    for (int i = threadIdx.x; i < N; i += blockDim.x)
+      st[i] = cmul_np(st[i], tab[2 * g.tot_edge - 2 * cut_count<WIDE>((g.x_hi | (uint64_t)i) ^ g.cmask, g)]);
+    __syncthreads();
+    const double c = rx[l].x, sn = rx[l].y;
+    for (int q = 0; q < n; ++q) {
+      for (int k = threadIdx.x; k < N / 2; k += blockDim.x) {
+        const int i0 = ((k >> q) << (q + 1)) | (k & ((1 << q) - 1));
+        double2 a = st[i0], b = st[i0 | (1 << q)];
+        rx_exact(a, b, c, sn);
+        st[i0] = a;
+        st[i0 | (1 << q)] = b;
+      }
+      __syncthreads();
+    }
+  }
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const double2 a = st[i];
+    amps[i] = a;
+    if (want_expect)
+      acc += (a.x * a.x + a.y * a.y) * (double)cut_count<WIDE>((g.x_hi | (uint64_t)i) ^ g.cmask, g);
+  }
+  if (want_expect) {
+    const double t = block_sum<kBlock>(acc, scratch);
+    if (threadIdx.x == 0) *expect_out = t;
+  }
+}
+
+cudaError_t launch_small_run(double2* amps, int n, const GraphDev& g, const double2* tables,
+                             const double2* rx, int p, int from_state, double u, int want_expect,
+                             double* expect_out, cudaStream_t s) {
+  if (n > 11) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(double2) << n;
+  if (g.n_nodes > 32)
+    small_run_kernel<true><<<1, kBlock, smem, s>>>(amps, n, g, tables, rx, p, from_state, u, want_expect,
+                                                   expect_out);
+  else
+    small_run_kernel<false><<<1, kBlock, smem, s>>>(amps, n, g, tables, rx, p, from_state, u, want_expect,
+                                                    expect_out);
+  return cudaGetLastError();
+}
+
 // ---- <C> reduction: expectation circuit.py:116-121 -------------------------
 template <bool WIDE>
 __global__ void expectation_kernel(const double2* __restrict__ amps, int n_local, GraphDev g,

@@ -83,6 +83,10 @@ cudaError_t launch_cost_gate(double2* amps, uint64_t n, const GraphDev& g, const
                              cudaStream_t s);
 cudaError_t launch_rx_gate(double2* amps, int n_local, int q, double c, double sn,
                            cudaStream_t s);
+// the whole p-level circuit for n <= 11 in one CTA (state in shared memory)
+cudaError_t launch_small_run(double2* amps, int n, const GraphDev& g, const double2* tables,
+                             const double2* rx, int p, int from_state, double u, int want_expect,
+                             double* expect_out, cudaStream_t s);
 cudaError_t launch_expectation(const double2* amps, int n_local, const GraphDev& g,
                                double* partials, int grid, cudaStream_t s);
 cudaError_t launch_norm_sq(const double2* amps, uint64_t n, double* partials, int grid,
