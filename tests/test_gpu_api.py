@@ -150,3 +150,64 @@ def test_expectation_only_run():
             _ = s.amps
         s2 = Q.simulate(g, pr, "bitwise", state=s, exact=exact)
         assert np.max(np.abs(s2.amps - full.amps)) <= 1e-12
+
+
+def test_new_entry_points_reject_bad_arguments():
+    """The segmented-run, exchange and weighted entry points fail with the
+    reference's exception types instead of launching."""
+    import ctypes
+
+    from paper_2312_03019_b200 import _lib
+
+    L = _lib.load()
+    g = Q.random_regular_graph(14, 3, seed=1)
+    eng = Q.Engine(14)
+    try:
+        eng.ensure_graph(g)
+        tables, cs, ss = Q.level_arrays(g, Q.params_from_seed(2, 0))
+        t = np.ascontiguousarray(tables)
+        nseg = ctypes.c_int()
+        with pytest.raises(RuntimeError):  # no planned run yet
+            eng.call("qaoa_run_segment", 0)
+        eng.call("qaoa_run_begin", 2, _lib.dptr(t.view(np.float64)), _lib.dptr(cs), _lib.dptr(ss),
+                 _lib.RUN_SHARDED, ctypes.byref(nseg))
+        assert nseg.value >= 2
+        with pytest.raises(IndexError):
+            eng.call("qaoa_run_segment", nseg.value)
+        with pytest.raises(IndexError):
+            eng.call("qaoa_run_sweep_range", 0, 0, 10 ** 6)
+        for k in range(nseg.value):
+            eng.call("qaoa_run_segment", k)
+        eng.call("qaoa_run_end")
+        with pytest.raises(RuntimeError):  # weights not set
+            eng.call("qaoa_run_layers_weighted", 1, _lib.dptr(np.array([0.3])), _lib.dptr(cs[:1]),
+                     _lib.dptr(ss[:1]), 0)
+        ptrs = (ctypes.c_void_p * 2)(eng.state_ptr(), eng.state_ptr())
+        with pytest.raises(ValueError):  # g = 5 > 4
+            _lib.check(L.qaoa_exchange(0, None, 5, ptrs, 14, 0, 0, 1, _lib.dptr(np.zeros(3)),
+                                       _lib.dptr(np.array([1.0, 0.0]))))
+        with pytest.raises(IndexError):  # swapped bits beyond the local qubits
+            _lib.check(L.qaoa_exchange(0, None, 1, ptrs, 14, 14, 0, 1, _lib.dptr(np.zeros(3)),
+                                       _lib.dptr(np.array([1.0, 0.0]))))
+    finally:
+        eng.close()
+
+
+def test_plan_export_matches_engine_launch_count():
+    """qaoa_plan (device-free) is the plan the engine runs: same sweep count."""
+    import ctypes
+
+    from paper_2312_03019_b200 import _lib
+
+    g = Q.random_regular_graph(30, 3, seed=0)
+    eng = Q.Engine(30)
+    try:
+        eng.ensure_graph(g)
+        tables, cs, ss = Q.level_arrays(g, Q.params_from_seed(10, 0))
+        t = np.ascontiguousarray(tables)
+        eng.call("qaoa_run_layers", 10, _lib.dptr(t.view(np.float64)), _lib.dptr(cs), _lib.dptr(ss), 0)
+        nl, hb = ctypes.c_int(), ctypes.c_double()
+        _lib.load().qaoa_last_run_stats(eng.ptr, ctypes.byref(nl), ctypes.byref(hb))
+        assert nl.value == _lib.load().qaoa_plan(30, 10, 0, None, 0) == 21
+    finally:
+        eng.close()
