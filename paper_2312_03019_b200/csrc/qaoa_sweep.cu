@@ -304,17 +304,4 @@ cudaError_t launch_sweep(const SweepArgs& a0, int grid, cudaStream_t stream) {
                           : launch_w<false>(a, grid, smem, stream);
 }
 
-int sweep_max_grid(int) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int sms = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int per_sm = 0;
-  const size_t smem = sweep_smem_bytes(0);
-  cudaFuncSetAttribute(sweep_kernel<false, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<false, 3, 2>, kThreads, smem);
-  if (per_sm < 1) per_sm = 1;
-  return sms * per_sm;
-}
-
 }  // namespace qb

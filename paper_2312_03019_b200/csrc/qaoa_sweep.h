@@ -75,7 +75,6 @@ void set_sweep_impl(int v);  // force 0 / 1 / 2, or 3 = per-sweep policy (defaul
 int sweep_grid(const SweepArgs& a);
 cudaError_t launch_sweep_tma(const SweepArgs& a, cudaStream_t stream);
 cudaError_t launch_sweep(const SweepArgs& args, int grid, cudaStream_t stream);
-int sweep_max_grid(int table_len);
 
 // simple (per-gate / per-element) kernels, qaoa_gates.cu
 cudaError_t launch_fill(double2* amps, uint64_t n, double2 v, cudaStream_t s);
