@@ -370,6 +370,10 @@ def run_sharded(args, rank: int, world: int, local: int):
             "gpu_launches": launches, "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
+    if hasattr(exch, "close"):
+        tdist.barrier()  # every rank is done with the peers' shards ...
+        exch.close()
+        tdist.barrier()  # ... and has unmapped them before any shard is freed
     shard.close()
     dist.destroy_process_group()
     return 0

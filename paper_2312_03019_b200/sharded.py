@@ -1,26 +1,30 @@
 """Multi-GPU QAOA: the 2^N state sharded over G = 2^g devices by its top g
 physical qubits (the reference has no distributed state,
-SPEC.md:186).
+SPEC.md:186).  Rank r holds physical indices [r 2^(N-g), (r+1) 2^(N-g)).
 
-Per level l (cost_l, then RX_l on every qubit):
-  1. every shard runs the fused engine on its N-g local qubits
-     (cost_l + RX_l, ``qaoa_run_layers`` with p=1) -- shard-local;
-  2. the g global physical bits are swapped with the top g local bits
-     (one all-to-all of G equal contiguous chunks: chunk d of rank r <-> chunk r
-     of rank d; (G-1)/G of each shard crosses the links);
-  3. the g qubits that just became local get RX_l in ONE fused sweep
-     (``qaoa_apply_rx_range``).
-The permutation is kept (never swapped back): ``ShardLayout.phys`` tracks the
-physical bit of every logical qubit, the cost kernels receive the graph's row
-masks relabelled to physical positions plus the shard's fixed high bits, and
-the fast-mode complement mask is permuted with the data.  <C> = fixed-rank-order
-sum of the shard partials (deterministic).
+The product path is ``simulate_sharded_fused``: every shard runs the planned
+fast schedule of its N-g local qubits in segments (``qaoa_run_begin`` /
+``qaoa_run_segment``), and once per level, right after the low set S_0
+(local bits 0..11), ONE in-place exchange pass swaps the g global bits with
+S_0's top g bits (chunk d of rank r <-> chunk r of rank d, (G-1)/G of each
+shard over the links) and applies that level's RX to the qubits that just
+became local (``qaoa_exchange`` kernel over peer pointers).  Exchangers:
+``IpcExchanger`` (one GPU per process, peers mapped with CUDA IPC, host
+barriers), ``IpcChunkExchanger`` (the same, pipelined chunk by chunk with
+inter-process CUDA events so the exchange overlaps the sweeps around it),
+``PeerExchanger`` / ``PeerChunkExchanger`` (G virtual shards on one device,
+for tests).
 
-Engines and exchangers are pluggable: ``CudaShard`` (the product: one engine
-context per shard) with ``DistExchanger`` (torch.distributed, NCCL over
-NVLink on a node, gloo on CPU) or ``LocalExchanger`` (G virtual shards in one
-process, device-to-device copies) -- the tests also drive this host logic with
-a CPU shard built on the oracle.
+``simulate_sharded`` is the unfused reference schedule (one engine run per
+level, then an all-to-all through ``DistExchanger`` -- torch.distributed P2P,
+NCCL on GPUs, gloo on CPU -- or ``LocalExchanger``, then one RX sweep over the
+arrived qubits); the tests also drive it with a CPU shard built on the oracle.
+
+Either way the permutation is kept (never swapped back): ``ShardLayout.phys``
+tracks the physical bit of every logical qubit, the cost kernels receive the
+graph's row masks relabelled to physical positions plus the shard's fixed high
+bits, and the fast-mode complement mask is permuted with the data.  <C> is the
+fixed-rank-order sum of the shard partials (deterministic).
 """
 
 from __future__ import annotations
