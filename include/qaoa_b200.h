@@ -116,6 +116,17 @@ QAOA_API int qaoa_apply_mixer(qaoa_ctx* ctx, double c, double s);
  * may toggle the range's bits in the complement mask, see qaoa_get_cmask). */
 QAOA_API int qaoa_apply_rx_range(qaoa_ctx* ctx, int q0, int count, double c, double s, int flags);
 
+/* Swapped qubit layout of fast unweighted runs (default -1: on for n >= 26 when
+ * the level-boundary merges alternate between two equal-size high qubit sets of
+ * 9 qubits (128-B runs; N=30) and a second state buffer fits with 4 GiB to
+ * spare; env QAOA_SWAP_LAYOUT=0 / 1 turns the policy off / on for every
+ * applicable size; mode 0: never; 1: whenever applicable).  Every low-set sweep then writes out of
+ * place with the two sets' bit ranges exchanged, so the top-bit set is always
+ * merged at bits 12..; runs end in identity order in the context's own buffer
+ * (bit-identical amplitudes; <C> partials summed in a different tile order).
+ * Costs a second 16 B x 2^n device buffer, kept until qaoa_destroy. */
+QAOA_API int qaoa_set_layout_swap(qaoa_ctx* ctx, int mode);
+
 /* Complement mask of the stored state: the amplitude of true basis index x is
  * stored at physical index x ^ cmask (fast-mode bookkeeping; bits >= n_local are
  * shard bits maintained by a sharded host).  read/write_amplitudes map the local

@@ -85,6 +85,13 @@ struct RunState {
   bool expect_fused = false;
   bool weighted = false;  // factored weighted cost (qaoa_run_layers_weighted)
   bool no_store_last = false;  // QAOA_RUN_EXPECT_ONLY
+  // swapped qubit layout (plan_swaps): lay[i] = layout sweep i reads (0: identity
+  // in amps, 1: bit ranges of sets 1 and last exchanged, in amps2); do_swap[i]:
+  // the (low-set) sweep writes out of place into the other layout
+  bool swap = false;
+  std::vector<uint8_t> lay, do_swap;
+  GraphDev g_sw;
+  int sw_lo = 0, sw_hi = 0, sw_m = 0;
 };
 
 }  // namespace
@@ -139,6 +146,9 @@ struct qaoa_ctx {
   double last_bytes = 0.0;
   RunState run;
   bool state_stale = false;  // last run skipped its final store (QAOA_RUN_EXPECT_ONLY)
+  // second state buffer of the swapped qubit layout (allocated on first use)
+  double2* amps2 = nullptr;
+  int swap_mode = -1;  // qaoa_set_layout_swap: -1 policy, 0 off, 1 whenever applicable
 };
 
 namespace {
@@ -193,11 +203,26 @@ std::vector<SetDesc> make_sets(int n) {
   const int rem = n - 12;
   if (rem <= 0) return sets;
   const int chunks = (rem + 8) / 9;  // at most 9 mixed bits per high sweep (C >= 3)
+  // the r = rem % chunks extra bits go to the middle chunks first, the ends
+  // taking two or none, so the first and last chunks (the level-boundary merges,
+  // see plan_swaps) have equal sizes whenever possible
+  const int r = rem % chunks;
+  std::vector<int> size(chunks, rem / chunks);
+  int mid = std::min(r, std::max(chunks - 2, 0));
+  if ((r - mid) % 2) --mid;
+  if (mid < 0 || r - mid > 2) {
+    for (int ci = 0; ci < r; ++ci) ++size[ci];  // two chunks, odd remainder
+  } else {
+    for (int ci = 0; ci < mid; ++ci) ++size[1 + ci];
+    if (r - mid == 2) {
+      ++size[0];
+      ++size[chunks - 1];
+    }
+  }
   int next = 12;
   for (int ci = 0; ci < chunks; ++ci) {
-    const int m = rem / chunks + (ci < rem % chunks ? 1 : 0);
-    sets.push_back(SetDesc{12 - m, next});
-    next += m;
+    sets.push_back(SetDesc{12 - size[ci], next});
+    next += size[ci];
   }
   return sets;
 }
@@ -273,6 +298,94 @@ void fill_graph(GraphDev& g, int n_nodes, const uint64_t* row_mask, int tot_edge
       m &= m - 1;
       g.adj[i] |= 1ull << j;
       g.adj[j] |= 1ull << i;
+    }
+  }
+}
+
+uint64_t swap_ranges_host(uint64_t x, int lo, int hi, int m) {
+  const uint64_t mask = (1ull << m) - 1ull;
+  const uint64_t a = (x >> lo) & mask, b = (x >> hi) & mask;
+  return (x & ~((mask << lo) | (mask << hi))) | (a << hi) | (b << lo);
+}
+
+// The graph with node (= physical bit) i relabelled to bit swap(i).
+GraphDev swap_graph(const GraphDev& g, int lo, int hi, int m) {
+  uint64_t rm[kMaxNodes] = {0};
+  for (int i = 0; i < g.n_nodes; ++i) {
+    uint64_t mk = g.rm[i];
+    while (mk) {
+      const int j = __builtin_ctzll(mk);
+      mk &= mk - 1;
+      int a = (int)__builtin_ctzll(swap_ranges_host(1ull << i, lo, hi, m));
+      int b = (int)__builtin_ctzll(swap_ranges_host(1ull << j, lo, hi, m));
+      if (a > b) std::swap(a, b);
+      rm[a] |= 1ull << b;
+    }
+  }
+  GraphDev out;
+  fill_graph(out, g.n_nodes, rm, g.tot_edge, g.x_hi);
+  out.cmask = swap_ranges_host(g.cmask, lo, hi, m);
+  return out;
+}
+
+// Swapped qubit layout (fast unweighted single-GPU runs).  The level-boundary
+// merges alternate between set 1 (physical bits 12..) and the last set (the
+// top bits, whose tiles touch one DRAM page per run: the slowest sweep kind).
+// Every low-set sweep S_0 -- contiguous 64 KiB tiles, its qubits 0..11 untouched
+// by the relabelling -- writes its tiles out of place with the bit ranges of set
+// 1 and the last set exchanged, so the set merged next always sits at bits
+// 12..: all merges run the set-1 geometry.  An even number of swaps per run
+// returns the state to identity order in its own buffer.
+void plan_swaps(qaoa_ctx* c, RunState& R) {
+  R.swap = false;
+  R.lay.assign(R.plan.size(), 0);
+  R.do_swap.assign(R.plan.size(), 0);
+  const int ns = (int)R.sets.size();
+  if (R.exact || R.weighted || R.sharded || ns < 3 || c->swap_mode == 0) return;
+  if (c->swap_mode < 0) {
+    static int env = -2;
+    if (env == -2) {
+      const char* e = getenv("QAOA_SWAP_LAYOUT");
+      env = e ? atoi(e) : -1;
+    }
+    if (env == 0) return;
+    // policy: states of >= 1 GiB whose top set has 128-B runs (C = 3: one DRAM
+    // page per run; N=30: +1.0-1.3% per step).  Sets with C >= 5 (N=31..33)
+    // measured no gain (profiles/r06_swap.md).
+    if (env < 0 && (c->n < 26 || R.sets[ns - 1].carry > 3)) return;
+  }
+  const int m1 = 12 - R.sets[1].carry, ml = 12 - R.sets[ns - 1].carry;
+  if (m1 != ml) return;
+  int n0 = 0;
+  for (const SweepPlan& sp : R.plan) n0 += sp.set == 0;
+  const int nswap = n0 & ~1;
+  if (nswap == 0) return;
+  if (!c->amps2) {
+    // only with room to spare (4 GiB beyond the buffer), else run in place
+    size_t free_b = 0, total_b = 0;
+    const size_t need = sizeof(double2) << c->n;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || free_b < need + (4ull << 30)) {
+      cudaGetLastError();
+      return;
+    }
+    if (cudaMalloc(&c->amps2, need) != cudaSuccess) {
+      cudaGetLastError();  // no room for the second buffer: run in place
+      c->amps2 = nullptr;
+      return;
+    }
+  }
+  R.swap = true;
+  R.sw_lo = R.sets[1].q;
+  R.sw_hi = R.sets[ns - 1].q;
+  R.sw_m = m1;
+  R.g_sw = swap_graph(c->g, R.sw_lo, R.sw_hi, R.sw_m);
+  int lay = 0, done = 0;
+  for (size_t i = 0; i < R.plan.size(); ++i) {
+    R.lay[i] = (uint8_t)lay;
+    if (R.plan[i].set == 0 && done < nswap) {
+      R.do_swap[i] = 1;
+      ++done;
+      lay ^= 1;
     }
   }
 }
@@ -492,6 +605,7 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
     CUDA_TRY(launch_wc_table(c->d_wc, c->d_wedge, c->d_w, c->n_wedges, sd.carry, sd.q, c->stream));
   }
   R.no_store_last = (flags & QAOA_RUN_EXPECT_ONLY) && R.expect_fused;
+  plan_swaps(c, R);
   R.active = true;
   if ((rc = record_event(c, R.timing, R.ev++))) return rc;
   return QAOA_OK;
@@ -504,11 +618,21 @@ int launch_plan_sweep(qaoa_ctx* c, int i, int64_t lo, int64_t cnt) {
   const int te = c->g.tot_edge + 1;
   const double u = sqrt(1.0 / (double)(1ull << c->g.n_nodes));
   const SweepPlan& sp = R.plan[i];
-  const SetDesc& st = R.sets[sp.set];
+  // swapped layout: sets 1 and last trade physical positions
+  const int ns = (int)R.sets.size();
+  const bool sw = R.swap && R.lay[i];
+  const int pset = !sw ? sp.set : sp.set == 1 ? ns - 1 : sp.set == ns - 1 ? 1 : sp.set;
+  const SetDesc& st = R.sets[pset];
   SweepArgs a;
   memset(&a, 0, sizeof(a));
-  a.amps = c->amps;
-  a.g = c->g;
+  a.amps = sw ? c->amps2 : c->amps;
+  a.g = sw ? R.g_sw : c->g;
+  if (R.swap && R.do_swap[i]) {
+    a.out = sw ? c->amps : c->amps2;
+    a.sw_lo = R.sw_lo;
+    a.sw_hi = R.sw_hi;
+    a.sw_m = R.sw_m;
+  }
   a.ntiles = 1ll << (c->n - 12);
   a.tile_lo = lo;
   a.tile_cnt = cnt;
@@ -657,6 +781,8 @@ void qaoa_destroy(qaoa_ctx* c) {
   if (c->d_winc) cudaFree(c->d_winc);
   if (c->d_wu) cudaFree(c->d_wu);
   if (c->d_wq) cudaFree(c->d_wq);
+  if (c->d_wc) cudaFree(c->d_wc);
+  if (c->amps2) cudaFree(c->amps2);
   for (auto e : c->events) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -785,6 +911,14 @@ int qaoa_read_amplitudes(qaoa_ctx* c, uint64_t offset, uint64_t count, double* d
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     permute_chunk((double2*)dst, all.data(), offset, count, m, 0);
   }
+  return QAOA_OK;
+}
+
+int qaoa_set_layout_swap(qaoa_ctx* c, int mode) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (mode < -1 || mode > 1) return fail(QAOA_E_INVALID, "layout swap mode must be -1, 0 or 1");
+  c->swap_mode = mode;
   return QAOA_OK;
 }
 

@@ -58,7 +58,15 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   const int tid = threadIdx.x;
   const int q = a.q;
   const uint64_t Q = 1ull << (C >= 12 ? 0 : q);
-  const uint64_t tile = (uint64_t)a.tile_lo + blockIdx.x;
+  // out-of-place swap sweeps visit tiles in an order whose consecutive blocks
+  // vary the low bits of BOTH swapped ranges, so the tiles in flight share a
+  // few DRAM pages on the read side and on the write side
+  auto visit = [&](uint64_t b) -> uint64_t {
+    if (C < 12 || !a.out) return b;
+    const int k = a.sw_m / 2 < 4 ? a.sw_m / 2 : 4;
+    return swap_bit_ranges(b, k, a.sw_hi - 12, k);
+  };
+  const uint64_t tile = visit((uint64_t)a.tile_lo + blockIdx.x);
   TileCtx tc;
   {
     const int low_bits = C >= 12 ? 0 : q - C;  // non-tile ranges [C, q) and [q + 12 - C, n)
@@ -80,14 +88,16 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
 #pragma unroll
     for (int r = 0; r < kRegs; ++r) v[r] = a.gen;
   } else {
-    if (a.pf_dist > 0 && tile + a.pf_dist < (uint64_t)(a.tile_lo + (a.tile_cnt ? a.tile_cnt : a.ntiles))) {
+    const uint64_t pf_b = (uint64_t)a.tile_lo + blockIdx.x + a.pf_dist;
+    if (a.pf_dist > 0 && pf_b < (uint64_t)(a.tile_lo + (a.tile_cnt ? a.tile_cnt : a.ntiles))) {
+      const uint64_t pf_tile = visit(pf_b);
       if (!a.pf_tensor) {
-        prefetch_tile_l2<C, kThreads>(amps, tile_base<C>(tile + a.pf_dist, q), Q, tid);
+        prefetch_tile_l2<C, kThreads>(amps, tile_base<C>(pf_tile, q), Q, tid);
       } else if (tid == 0) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           int c[5];
-          half_coords<C>(a, tile + a.pf_dist, h, c);
+          half_coords<C>(a, pf_tile, h, c);
           asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
                            reinterpret_cast<uint64_t>(&a.map)),
                        "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4])
@@ -145,7 +155,13 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     constexpr int last = fast_last<C, FLOW>();
     if (flags & kExpect)
       acc = WGT ? expect_wacc<last>(v, &wcb[0], a.wc, tid, sk) : expect_acc<last>(v, &cb, tid, sk);
-    store_tile<C, last>(amps, tc, Q, v, flags, sk);
+    if (C >= 12 && a.out) {  // out of place into the swapped qubit layout
+      TileCtx to = tc;
+      to.base = swap_bit_ranges(tc.base, a.sw_lo, a.sw_hi, a.sw_m);
+      store_tile<C, last>(a.out, to, Q, v, flags, sk);
+    } else {
+      store_tile<C, last>(amps, tc, Q, v, flags, sk);
+    }
   }
   if (flags & kExpect) {
     const double t = block_sum<kThreads>(acc, red_scratch);

@@ -53,6 +53,11 @@ struct SweepArgs {
   int wm;
   const double* ww;      // [wm] edge weights (weighted <C>)
   const double* wc;      // 4096-entry tile-internal cut weight table of the last sweep's set
+  // out-of-place low-set sweep (C = 12, one tile per CTA): tile stored to `out`
+  // with physical index bits [sw_lo, sw_lo + sw_m) and [sw_hi, sw_hi + sw_m)
+  // swapped (the swapped qubit layout of qaoa_capi.cu); nullptr = in place
+  double2* out;
+  int sw_lo, sw_hi, sw_m;
 };
 // Tile-internal phase table of one weighted cost level for tile geometry (C, q):
 // Q[t] = scale * prod over edges with both endpoints tile nodes of u_e (equal

@@ -193,6 +193,13 @@ __device__ __forceinline__ void half_coords(const SweepArgs& a, uint64_t tile, i
     }
   }
 }
+// x with bit ranges [lo, lo + m) and [hi, hi + m) exchanged (disjoint ranges).
+__device__ __forceinline__ uint64_t swap_bit_ranges(uint64_t x, int lo, int hi, int m) {
+  const uint64_t mask = (1ull << m) - 1ull;
+  const uint64_t a = (x >> lo) & mask, b = (x >> hi) & mask;
+  return (x & ~((mask << lo) | (mask << hi))) | (a << hi) | (b << lo);
+}
+
 struct TileCtx {
   uint64_t base;           // physical index of tile element 0 (tile bits zero), without x_hi
   uint64_t tb0, tb1, tb2;  // thread base offsets per mapping

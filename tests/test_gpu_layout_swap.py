@@ -1,0 +1,124 @@
+"""Swapped qubit layout (qaoa_set_layout_swap, qaoa_capi.cu plan_swaps): every
+low-set sweep writes its tiles out of place with the bit ranges of the two
+alternately merged high sets exchanged.  Same arithmetic at other addresses, so
+the amplitudes must be bit-identical to the in-place run; <C> agrees up to the
+order its per-tile partials are summed in."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2312_03019_b200 as Q
+from paper_2312_03019_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(eng, g, params, mode, flags=0):
+    eng.call("qaoa_set_layout_swap", mode)
+    tables, cs, ss = Q.level_arrays(g, params)
+    t = np.ascontiguousarray(tables)
+    eng.call("qaoa_run_layers", params.p, _lib.dptr(t.view(np.float64)), _lib.dptr(cs),
+             _lib.dptr(ss), flags | _lib.RUN_EXPECTATION)
+    return eng.scalar("qaoa_expectation")
+
+
+def _state(eng, n):
+    import torch
+
+    from paper_2312_03019_b200.state import _wrap_device
+
+    return _wrap_device(eng.state_ptr(), 16 << n, 0).view(torch.complex128).clone()
+
+
+def _stats(eng):
+    nl, hb = ctypes.c_int(), ctypes.c_double()
+    _lib.load().qaoa_last_run_stats(eng.ptr, ctypes.byref(nl), ctypes.byref(hb))
+    return nl.value, hb.value
+
+
+@pytest.mark.parametrize("n", [22, 23, 24])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+def test_swapped_layout_bit_identical(n, p):
+    """n = 22 / 24: high sets 5+5 / 6+6 (swap applies); n = 23: 6+5 (it does
+    not, mode 1 must fall back to in place).  Angle seeds mix both RX forms."""
+    import torch
+
+    g = Q.random_regular_graph(n, 3, seed=1) if n % 2 == 0 else \
+        Q.erdos_renyi_graph(n, 0.2, seed=1)
+    eng = Q.Engine(n)
+    try:
+        eng.ensure_graph(g)
+        for seed in (0, 3):
+            params = Q.params_from_seed(p, seed)
+            e0 = _run(eng, g, params, 0)
+            s0, st0 = _state(eng, n), _stats(eng)
+            e1 = _run(eng, g, params, 1)
+            s1, st1 = _state(eng, n), _stats(eng)
+            assert torch.equal(s0, s1), (n, p, seed)
+            assert e1 == pytest.approx(e0, rel=1e-13, abs=1e-13)
+            assert st0 == st1
+    finally:
+        eng.close()
+
+
+def test_swapped_layout_continuation_and_expect_only():
+    """FROM_STATE continuation (a complement mask carried in) and an
+    expectation-only last sweep through the swapped layout."""
+    import torch
+
+    n = 24
+    g = Q.random_regular_graph(n, 3, seed=2)
+    eng = Q.Engine(n)
+    try:
+        eng.ensure_graph(g)
+        pa, pb = Q.params_from_seed(3, 5), Q.params_from_seed(4, 6)
+        out = {}
+        for mode in (0, 1):
+            _run(eng, g, pa, mode)
+            e = _run(eng, g, pb, mode, _lib.RUN_FROM_STATE)
+            out[mode] = (_state(eng, n), e)
+            e_only = _run(eng, g, pb, mode, _lib.RUN_FROM_STATE | _lib.RUN_EXPECT_ONLY)
+            assert np.isfinite(e_only)
+        assert torch.equal(out[0][0], out[1][0])
+        assert out[1][1] == pytest.approx(out[0][1], rel=1e-13)
+    finally:
+        eng.close()
+
+
+def test_swapped_layout_policy_and_buffer():
+    """Default policy: on for n >= 26 (one extra state buffer, allocated once);
+    results equal the in-place run; ⟨C⟩ matches the reference's golden value at
+    BASELINE configs[1] (u3r N=26 seed 0, p=4: 17.687434636566532)."""
+    import torch
+
+    n = 26
+    g = Q.random_regular_graph(n, 3, seed=0)
+    eng = Q.Engine(n)
+    try:
+        eng.ensure_graph(g)
+        params = Q.params_from_seed(4, 0)
+        e_in = _run(eng, g, params, 0)
+        s_in = _state(eng, n)
+        free0 = torch.cuda.mem_get_info()[0]
+        e_pol = _run(eng, g, params, -1)
+        free1 = torch.cuda.mem_get_info()[0]
+        assert free0 - free1 >= 16 << n  # the second buffer
+        assert torch.equal(_state(eng, n), s_in)
+        assert e_pol == pytest.approx(17.687434636566532, rel=1e-10)
+        assert e_in == pytest.approx(17.687434636566532, rel=1e-10)
+        free2 = torch.cuda.mem_get_info()[0]
+        _run(eng, g, params, -1)
+        assert torch.cuda.mem_get_info()[0] >= free2 - (64 << 20)  # reused, not reallocated
+    finally:
+        eng.close()
+
+
+def test_layout_swap_rejects_bad_mode():
+    eng = Q.Engine(14)
+    try:
+        with pytest.raises(ValueError):
+            eng.call("qaoa_set_layout_swap", 2)
+    finally:
+        eng.close()
