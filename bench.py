@@ -449,9 +449,10 @@ def run_ours(args, rank: int, world: int, local: int):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "peak_kind": peak_kind,
-                "kernel": "fused cost+RX sweeps (qb::sweep_kernel one tile per CTA + L2 prefetch; "
-                          "qb::sweep_tma_kernel persistent TMA-fed for the launch-control and "
-                          "top-set merged sweeps)",
+                "kernel": "fused cost+RX sweeps (qb::sweep_kernel one tile per CTA + L2 prefetch, "
+                          "low-set sweeps out of place into the swapped qubit layout; "
+                          "qb::sweep_tma_kernel persistent TMA-fed for the launch-control sweep "
+                          "and merges on a top set)",
                 "launch_ms_last_step": [round(x, 3) for x in launch_ms[-sweeps_per_step:]],
                 "algorithmic_bytes_per_launch": 32 * (1 << n),
                 "launches_per_step": sweeps_per_step,
