@@ -80,3 +80,21 @@ def test_plan_is_the_circuit(n, p, flags):
         assert len(rows) == (R - 1) * p + 1  # level-boundary merges
     elif flags & EXACT:
         assert len(rows) == R * p
+
+
+@pytest.mark.parametrize("n", range(22, 41))
+def test_merged_high_sets_have_equal_sizes(n):
+    """make_sets gives the extra qubits to the middle high sets first, so the
+    two sets merged at level boundaries (the first and last high sets) have the
+    same size -- the condition of the swapped qubit layout -- except with two
+    high sets and an odd remainder (N = 23, 25, 27, 29)."""
+    rows = plan(n, 4, 0)
+    sets = sorted({(q, carry) for carry, q, *_ in rows if carry < 12})
+    sizes = [12 - carry for _, carry in sets]
+    assert sum(sizes) == n - 12 and max(sizes) <= 9
+    assert max(sizes) - min(sizes) <= 1
+    if len(sizes) >= 3 or (n - 12) % 2 == 0:
+        assert sizes[0] == sizes[-1]
+    # the merged sweeps are exactly the first and last high sets
+    merged = {(q, carry) for carry, q, pre, s1, mid, s2, ex in rows if s2 >= 0}
+    assert merged == {sets[0], sets[-1]}
