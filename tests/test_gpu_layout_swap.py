@@ -87,10 +87,11 @@ def test_swapped_layout_continuation_and_expect_only():
         eng.close()
 
 
-def test_swapped_layout_policy_and_buffer():
-    """Default policy: on for n >= 26 (one extra state buffer, allocated once);
-    results equal the in-place run; ⟨C⟩ matches the reference's golden value at
-    BASELINE configs[1] (u3r N=26 seed 0, p=4: 17.687434636566532)."""
+def test_swapped_layout_buffer_and_golden():
+    """Mode 1 at BASELINE configs[1] (u3r N=26 seed 0, p=4): one extra state
+    buffer, allocated once; amplitudes equal the in-place run; <C> is the
+    reference's golden 17.687434636566532.  The default policy leaves N=26
+    (7-qubit high sets, C = 5) in place."""
     import torch
 
     n = 26
@@ -102,15 +103,37 @@ def test_swapped_layout_policy_and_buffer():
         e_in = _run(eng, g, params, 0)
         s_in = _state(eng, n)
         free0 = torch.cuda.mem_get_info()[0]
-        e_pol = _run(eng, g, params, -1)
+        _run(eng, g, params, -1)
+        assert torch.cuda.mem_get_info()[0] >= free0 - (64 << 20)  # policy: in place here
+        e_sw = _run(eng, g, params, 1)
         free1 = torch.cuda.mem_get_info()[0]
         assert free0 - free1 >= 16 << n  # the second buffer
         assert torch.equal(_state(eng, n), s_in)
-        assert e_pol == pytest.approx(17.687434636566532, rel=1e-10)
+        assert e_sw == pytest.approx(17.687434636566532, rel=1e-10)
         assert e_in == pytest.approx(17.687434636566532, rel=1e-10)
         free2 = torch.cuda.mem_get_info()[0]
-        _run(eng, g, params, -1)
+        _run(eng, g, params, 1)
         assert torch.cuda.mem_get_info()[0] >= free2 - (64 << 20)  # reused, not reallocated
+    finally:
+        eng.close()
+
+
+def test_swapped_layout_default_at_n30():
+    """The bench configuration (u3r N=30, 9-qubit high sets): the default
+    policy swaps (second 16 GiB buffer) and gives the in-place <C>."""
+    import torch
+
+    n = 30
+    g = Q.random_regular_graph(n, 3, seed=0)
+    eng = Q.Engine(n)
+    try:
+        eng.ensure_graph(g)
+        params = Q.params_from_seed(3, 0)
+        e_in = _run(eng, g, params, 0)
+        free0 = torch.cuda.mem_get_info()[0]
+        e_pol = _run(eng, g, params, -1)
+        assert free0 - torch.cuda.mem_get_info()[0] >= 16 << n
+        assert e_pol == pytest.approx(e_in, rel=1e-13)
     finally:
         eng.close()
 
