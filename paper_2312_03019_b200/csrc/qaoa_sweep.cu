@@ -293,6 +293,10 @@ static int pf_distance(const SweepArgs& a) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // out-of-place low-set sweeps: their writes allocate fresh L2 lines, and a
+  // prefetch two waves ahead was partly evicted before use (+2% DRAM reads);
+  // half a wave ahead measured best (S0 5.27 vs 5.35-5.41 ms, profiles/r06_swap.md)
+  if (a.out) return sms / 2;
   return 2 * sms;
 }
 
