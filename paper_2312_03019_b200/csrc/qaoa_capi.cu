@@ -1219,6 +1219,10 @@ int qaoa_run_sweep_range(qaoa_ctx* c, int i, int64_t tile_lo, int64_t tile_count
   const int64_t nt = 1ll << (c->n - 12);
   if (tile_lo < 0 || tile_count < 1 || tile_lo + tile_count > nt)
     return fail(QAOA_E_RANGE, "tile range out of range");
+  // an out-of-place sweep of the swapped layout visits its tiles in a permuted
+  // order over the whole state: no partial ranges (sharded runs never swap)
+  if (R.swap && R.do_swap[i] && (tile_lo != 0 || tile_count != nt))
+    return fail(QAOA_E_STATE, "partial tile ranges need an in-place run (qaoa_set_layout_swap(ctx, 0))");
   return launch_plan_sweep(c, i, tile_lo, tile_count);
 }
 
