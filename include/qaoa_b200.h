@@ -246,7 +246,9 @@ QAOA_API int qaoa_run_end(qaoa_ctx* ctx);
  * that the top index bits not mixed by the sweep are the top tile-index bits.
  * qaoa_run_sweep_range launches sweep i on tiles [tile_lo, tile_lo + count)
  * instead of inside qaoa_run_segment (the caller runs every sweep of the
- * segment exactly once, in order per tile). */
+ * segment exactly once, in order per tile).  Unsharded runs that use the
+ * swapped layout (qaoa_set_layout_swap) refuse partial ranges of their
+ * out-of-place low-set sweeps (QAOA_E_STATE). */
 QAOA_API int qaoa_run_sweep_info(qaoa_ctx* ctx, int i, int* segment, int* carry, int* q,
                                  int64_t* ntiles);
 QAOA_API int qaoa_run_sweep_range(qaoa_ctx* ctx, int i, int64_t tile_lo, int64_t tile_count);

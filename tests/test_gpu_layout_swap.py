@@ -145,3 +145,43 @@ def test_layout_swap_rejects_bad_mode():
             eng.call("qaoa_set_layout_swap", 2)
     finally:
         eng.close()
+
+
+def test_swapped_layout_refuses_partial_ranges_of_out_of_place_sweeps():
+    """qaoa_run_sweep_range on an unsharded swapped run: whole ranges work (the
+    result equals qaoa_run_layers), a partial range of an out-of-place low-set
+    sweep is refused instead of visiting the wrong tiles."""
+    import torch
+
+    from paper_2312_03019_b200._lib import EngineError
+
+    n, p = 24, 2
+    g = Q.random_regular_graph(n, 3, seed=4)
+    params = Q.params_from_seed(p, 2)
+    tables, cs, ss = Q.level_arrays(g, params)
+    t = np.ascontiguousarray(tables)
+    eng = Q.Engine(n)
+    try:
+        eng.ensure_graph(g)
+        _run(eng, g, params, 1)
+        ref = _state(eng, n)
+        nseg = ctypes.c_int()
+        eng.call("qaoa_run_begin", p, _lib.dptr(t.view(np.float64)), _lib.dptr(cs), _lib.dptr(ss),
+                 0, ctypes.byref(nseg))
+        L = _lib.load()
+        i = 0
+        while True:
+            seg, carry, q, nt = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+            rc = L.qaoa_run_sweep_info(eng.ptr, i, ctypes.byref(seg), ctypes.byref(carry),
+                                       ctypes.byref(q), ctypes.byref(nt))
+            if rc == _lib.QAOA_E_RANGE:
+                break
+            if carry.value == 12:  # the out-of-place low-set sweep
+                with pytest.raises(EngineError, match="partial"):
+                    eng.call("qaoa_run_sweep_range", i, 0, nt.value // 2)
+            eng.call("qaoa_run_sweep_range", i, 0, nt.value)
+            i += 1
+        eng.call("qaoa_run_end")
+        assert torch.equal(_state(eng, n), ref)
+    finally:
+        eng.close()
