@@ -21,6 +21,12 @@ for n in (5, 12, 13, 15, 16, 21):
     Q.apply_mixer_layer(s, 0.3)
     Q.apply_cost_layer(s, g, 0.4, "bitwise")
     Q.apply_rx(s, n - 1, 0.2)
+# swapped qubit layout: out-of-place low-set sweeps (n = 22: high sets 5 + 5)
+g = Q.random_regular_graph(22, 3, seed=2)
+s = Q.init_uniform(22, max_qubits=22)
+s.engine().call("qaoa_set_layout_swap", 1)
+s = Q.simulate(g, Q.QaoaParams((0.3, 1.2), (0.5, 2.9)), "bitwise", max_qubits=22, state=s)
+Q.expectation(g, s)
 g = Q.random_regular_graph(16, 3, seed=1)
 shards = [CudaShard(14, r) for r in range(4)]
 simulate_sharded(g, Q.QaoaParams((0.3, 1.0), (2.9, 0.4)), shards, LocalExchanger(shards), 2)
