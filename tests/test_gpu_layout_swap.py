@@ -185,3 +185,32 @@ def test_swapped_layout_refuses_partial_ranges_of_out_of_place_sweeps():
         assert torch.equal(_state(eng, n), ref)
     finally:
         eng.close()
+
+
+def test_swapped_layout_with_partial_complement_mask():
+    """A complement mask that is not swap-invariant (bits in only one of the
+    two exchanged ranges, as qaoa_set_cmask / qaoa_apply_rx_range can leave)
+    is permuted with the data: swapped == in place, and the mask is unchanged
+    after the run (even number of swaps)."""
+    import torch
+
+    n = 24  # high sets: bits 12..17 and 18..23
+    g = Q.random_regular_graph(n, 3, seed=5)
+    eng = Q.Engine(n)
+    try:
+        eng.ensure_graph(g)
+        pa, pb = Q.params_from_seed(2, 7), Q.params_from_seed(3, 8)
+        cm = (0b101 << 13) | (1 << 4)  # bits 4, 13, 15
+        out = {}
+        for mode in (0, 1):
+            _run(eng, g, pa, 0)
+            eng.call("qaoa_set_cmask", cm)
+            e = _run(eng, g, pb, mode, _lib.RUN_FROM_STATE)
+            m = ctypes.c_uint64()
+            eng.call("qaoa_get_cmask", ctypes.byref(m))
+            out[mode] = (_state(eng, n), e, m.value)
+        assert torch.equal(out[0][0], out[1][0])
+        assert out[1][1] == pytest.approx(out[0][1], rel=1e-13)
+        assert out[0][2] == out[1][2]
+    finally:
+        eng.close()
