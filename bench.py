@@ -502,7 +502,11 @@ def run_ours(args, rank: int, world: int, local: int):
         h2d = 8 * n + tables.nbytes + cs.nbytes + ss.nbytes
         e2e = {"value": world * p * args.e2e_steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8,
-               "api": "paper_2312_03019_b200.simulate + expectation"}
+               "api": "paper_2312_03019_b200.simulate + expectation",
+               # a separate timed loop (wall clock, host inputs): the sweeps run at
+               # the board power limit, so it can land a little above `value`
+               # (whose loop also records per-sweep events) -- same kernels
+               "steps": args.e2e_steps}
         assert abs(val - expect_val) <= 1e-10 * abs(expect_val)
 
     cpu = None
