@@ -150,6 +150,33 @@ def norm(n: int, amps: np.ndarray, threads: int = 0) -> float:
     return float(lib().orc_norm(n, _ptr(amps, _f64p), threads))
 
 
+def simulate_slice(n_local: int, n_nodes: int, row_mask, x_hi: int, tot_edge: int, gammas, betas,
+                   threads: int = 0) -> np.ndarray:
+    """The 2^n_local amplitudes of a graph with n_nodes > n_local nodes whose top
+    node bits are fixed to x_hi (one shard's index space, no RX on the fixed
+    bits): init u = sqrt(1/2^n_nodes) (circuit.py:45), then per level the
+    bitwise cost at x_hi | y (cost.py:162-176) and the mixer on the n_local
+    qubits (circuit.py:89-94).  Checks the engine's 64-bit-mask path
+    (graph.py:41-42 allows N <= 64) on a slice a CPU can hold."""
+    a = np.full(1 << n_local, math.sqrt(1.0 / (1 << n_nodes)), dtype=np.complex128)
+    m = _masks(row_mask)
+    for gm, bt in zip(gammas, betas):
+        tab = np.ascontiguousarray(phase_table(tot_edge, gm))
+        lib().orc_apply_cost_x(n_local, n_nodes, _ptr(m, _u64p), x_hi, tot_edge, _ptr(tab, _f64p),
+                               _ptr(a, _f64p), threads)
+        c, s = rx_coeffs(bt)
+        lib().orc_apply_mixer(n_local, c, s, _ptr(a, _f64p), threads)
+    return a
+
+
+def expectation_slice(n_local: int, n_nodes: int, row_mask, x_hi: int, amps: np.ndarray,
+                      threads: int = 0) -> float:
+    """sum_y |a_y|^2 C(x_hi | y) (circuit.py:116-121 restricted to one slice)."""
+    m = _masks(row_mask)
+    return float(lib().orc_expectation_x(n_local, n_nodes, _ptr(m, _u64p), x_hi,
+                                         _ptr(amps, _f64p), threads))
+
+
 class OracleShard:
     """CPU shard for the sharded-host tests (paper_2312_03019_b200.sharded.Shard
     protocol): reference arithmetic on a numpy shard of global indices x_hi | y."""

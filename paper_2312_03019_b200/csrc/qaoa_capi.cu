@@ -549,7 +549,6 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
     const size_t nq = (size_t)p * 4096;
     if (c->d_wq_cap < nq) {
       if (c->d_wq) cudaFree(c->d_wq);
-  if (c->d_wc) cudaFree(c->d_wc);
       c->d_wq = nullptr;
       c->d_wq_cap = 0;
       CUDA_TRY(cudaMalloc(&c->d_wq, nq * sizeof(double2)));

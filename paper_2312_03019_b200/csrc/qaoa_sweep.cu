@@ -228,12 +228,15 @@ size_t sweep_smem_bytes(int) { return (size_t)kSlots * sizeof(double2); }
 
 template <bool WIDE, int C, int FLOW, bool WGT = false>
 static cudaError_t launch_one(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {
-  static bool configured = false;  // per instantiation
-  if (!configured) {
+  static unsigned long long configured = 0;  // per instantiation, bit d = device d done
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(sweep_kernel<WIDE, C, FLOW, WGT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
   }
   sweep_kernel<WIDE, C, FLOW, WGT><<<grid, kThreads, smem, s>>>(a);
   return cudaGetLastError();

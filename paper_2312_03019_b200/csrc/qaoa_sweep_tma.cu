@@ -373,12 +373,15 @@ int num_sms() {
 
 template <bool WIDE, int C, int FLOW, bool TS>
 cudaError_t launch_tma_one(const TmaSweepArgs& ta, int grid, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;  // bit d = device d done
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(sweep_tma_kernel<WIDE, C, FLOW, TS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
   }
   sweep_tma_kernel<WIDE, C, FLOW, TS><<<grid, kCtaThreads, kTmaSmem, s>>>(ta);
   return cudaGetLastError();

@@ -239,3 +239,19 @@ def test_pack_unpack_chunks_roundtrip():
     torch.cuda.synchronize()
     s._where = "device"
     assert np.array_equal(s.amps, amps)
+
+
+def test_weighted_fused_regrow_tables_on_one_state():
+    """Fused weighted runs with growing p on one reused state (the per-level
+    tile tables grow; the <C> table must survive the regrow): p=1, then p=3,
+    then p=2 each equal a fresh context's run (regression: a freed <C> table
+    pointer was reused after the per-level tables grew)."""
+    g = Q.random_regular_graph(16, 3, seed=4, weighted=True)
+    s = None
+    for gm, bt in (((0.7,), (0.4,)), ((0.3, 1.9, 0.8), (0.2, 2.7, 1.1)), ((1.2, 0.5), (0.9, 0.3))):
+        pr = Q.QaoaParams(gm, bt)
+        s = Q.simulate(g, pr, "compressed", state=s)
+        e = Q.expectation(g, s)
+        fresh = Q.simulate(g, pr, "compressed")
+        assert Q.max_abs_diff(s, fresh) == 0.0
+        assert e == Q.expectation(g, fresh)

@@ -1,0 +1,283 @@
+"""GPU parity above 32 nodes and at the north-star configs the CPU cannot hold.
+
+* Graphs wider than 32 nodes (64-bit row masks, reference graph.py:41-42 allows
+  N <= 64) through the fused sweeps and <C>: a 2^20 slice with the top node
+  bits fixed (x_hi) against the oracle restricted to that slice
+  (oracle.simulate_slice), exact schedule bit for bit, fast within 1e-12.
+* Config C4 (BASELINE configs[3]): ER(0.5) N=33 seed 0, E=236, 128 GiB state on
+  one GPU -- p=1 per-edge closed form, exact vs fast schedule through strided
+  host samples and <C>, norm, 0 <= <C> <= E, cut-table invariants at 2^33
+  states, 16 virtual shards (x_hi reaches bit 32) against the unsharded run.
+* Config C3 (configs[2]): u3r N=30 p=10 against the oracle port run on the
+  host: exact state bit-identical over all 2^30 amplitudes, fast within 1e-12.
+
+Tolerances are the north star's: amplitudes 1e-12 absolute, <C> 1e-10 relative.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2312_03019_b200 as Q
+from paper_2312_03019_b200 import _lib
+from paper_2312_03019_b200.circuit import level_arrays
+
+pytestmark = pytest.mark.gpu
+
+AMP_TOL = 1e-12
+EXP_RTOL = 1e-10
+
+
+def _cut_counts_numpy(row_mask, xs):
+    """C(x) = sum_i popcount(row_mask[i] & (bcast(x_i) ^ x)) (cost.py:55-63, 88-99)."""
+    c = np.zeros(xs.size, dtype=np.int64)
+    for i, m in enumerate(row_mask):
+        b = np.uint64(0) - ((xs >> np.uint64(i)) & np.uint64(1))
+        c += np.bitwise_count(np.uint64(m) & (b ^ xs)).astype(np.int64)
+    return c
+
+
+def _free_gib():
+    import torch
+
+    free, _ = torch.cuda.mem_get_info(0)
+    return free / 2**30
+
+
+def _run_slice(g, n_local, x_hi, pr, exact):
+    eng = Q.Engine(n_local)
+    try:
+        masks = np.ascontiguousarray(np.array(g.row_mask, dtype=np.uint64))
+        eng.call("qaoa_set_graph", g.n, masks.ctypes.data_as(_lib._u64p), g.tot_edge, int(x_hi))
+        tables, cs, ss = level_arrays(g, pr)
+        flags = _lib.RUN_EXPECTATION | (_lib.RUN_EXACT if exact else 0)
+        eng.call("qaoa_run_layers", pr.p, _lib.dptr(tables.view(np.float64)), _lib.dptr(cs),
+                 _lib.dptr(ss), flags)
+        e = eng.scalar("qaoa_expectation")
+        return eng.read(), e
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("n_nodes,kind,n_local", [
+    (34, "u3r", 20),   # 64-bit masks, uint8 phases (E=51)
+    (40, "er", 20),    # dense: E > 255 (uint16-class graph), 4-set geometry at n_local=23
+    (40, "er", 23),
+    (64, "u3r", 21),   # the widest graph the reference allows; x_hi reaches bit 63
+])
+def test_wide_graph_slice_vs_oracle(oracle, n_nodes, kind, n_local):
+    """Fused sweeps + fused <C> with n_nodes > 32 on one slice x_hi | y: exact
+    schedule == oracle bit for bit, fast within 1e-12 (betas <= pi/2 keep every
+    level in the first RX form, so no complement of the fixed bits is needed)."""
+    g = Q.random_regular_graph(n_nodes, 3, seed=5) if kind == "u3r" else \
+        Q.erdos_renyi_graph(n_nodes, 0.5, seed=3)
+    rng = np.random.default_rng(n_nodes + n_local)
+    pr = Q.QaoaParams((0.37, 1.21, 2.6), (0.9, 0.31, 1.4))
+    for _ in range(2):
+        x_hi = int(rng.integers(0, 1 << (n_nodes - n_local), dtype=np.uint64)) << n_local
+        if n_nodes == 64:
+            x_hi |= 1 << 63
+        ref = oracle.simulate_slice(n_local, n_nodes, g.row_mask, x_hi, g.tot_edge, pr.gamma, pr.beta)
+        eref = oracle.expectation_slice(n_local, n_nodes, g.row_mask, x_hi, ref)
+        ex, ee = _run_slice(g, n_local, x_hi, pr, exact=True)
+        assert np.array_equal(ex, ref), (n_nodes, hex(x_hi))
+        assert ee == pytest.approx(eref, rel=EXP_RTOL)
+        fa, fe = _run_slice(g, n_local, x_hi, pr, exact=False)
+        assert np.max(np.abs(fa - ref)) <= AMP_TOL, (n_nodes, hex(x_hi))
+        assert fe == pytest.approx(eref, rel=EXP_RTOL)
+
+
+# ---- config C4: ER(0.5) N=33 seed 0 on one GPU ------------------------------
+N33 = 33
+C4_EXPECTED_E = 236
+BLOCKS = 64
+BLOCK = 4096
+
+
+def _c4_graph():
+    g = Q.erdos_renyi_graph(N33, 0.5, seed=0)
+    assert g.tot_edge == C4_EXPECTED_E
+    return g
+
+
+def _sample_offsets(n):
+    rng = np.random.default_rng(33)
+    size = 1 << n
+    offs = [0, size - BLOCK]
+    for k in range(BLOCKS - 2):
+        lo = k * (size // (BLOCKS - 2))
+        offs.append(lo + int(rng.integers(0, size // (BLOCKS - 2) - BLOCK)))
+    return sorted(offs)
+
+
+def _host_sample(eng, offsets):
+    return np.concatenate([eng.read(o, BLOCK) for o in offsets])
+
+
+def _need(gib):
+    if _free_gib() < gib:
+        pytest.skip(f"needs {gib} GiB of free device memory")
+
+
+def _c4_run(g, pr, exact):
+    s = Q.simulate(g, pr, "bitwise", exact=exact, max_qubits=N33)
+    try:
+        e = Q.expectation(g, s)
+        nrm = s.norm()
+        sample = _host_sample(s.engine(), _sample_offsets(N33))
+    finally:
+        s.engine().close()
+    return sample, e, nrm
+
+
+@pytest.fixture(scope="module")
+def c4_fast_p4():
+    _need(130)
+    g = _c4_graph()
+    pr = Q.params_from_seed(4, 0)
+    return _c4_run(g, pr, exact=False)
+
+
+def test_c4_p1_closed_form():
+    """p=1 per-edge closed form (any graph) at ER N=33."""
+    _need(130)
+    from oracle import oracle as O
+
+    g = _c4_graph()
+    gm, bt = O.params_from_seed(1, 0)
+    cf = O.p1_closed_form(N33, [(i, j) for i, j, _ in g.edges], gm[0], bt[0])
+    s = Q.simulate(g, Q.QaoaParams(gm, bt), "bitwise", max_qubits=N33)
+    try:
+        e = Q.expectation(g, s)
+        assert e == pytest.approx(cf, rel=EXP_RTOL)
+        assert s.norm() == pytest.approx(1.0, abs=1e-12)
+    finally:
+        s.engine().close()
+
+
+def test_c4_exact_vs_fast_p4(c4_fast_p4):
+    """Config C4 at p=4: the bit-exact schedule (the reference's qubit order
+    and rounding) against the fast one, through 64 blocks of 4096 amplitudes
+    spread over the 2^33 indices plus <C>; norm 1; 0 <= <C> <= E."""
+    g = _c4_graph()
+    pr = Q.params_from_seed(4, 0)
+    fs, fe, fn = c4_fast_p4
+    es, ee, en = _c4_run(g, pr, exact=True)
+    assert np.max(np.abs(es - fs)) <= AMP_TOL
+    assert fe == pytest.approx(ee, rel=EXP_RTOL)
+    assert fn == pytest.approx(1.0, abs=1e-12) and en == pytest.approx(1.0, abs=1e-12)
+    assert 0.0 <= fe <= g.tot_edge
+    # sample norms are consistent with a normalised state (no blocks of zeros)
+    assert np.all(np.abs(fs) > 0)
+
+
+def test_c4_cut_table_invariants():
+    """K1 at 2^33 states (uint8 table, 8 GiB): sum_x C(x) = E 2^32, C(x) = C(~x)
+    on sampled ranges, bit-exact against the numpy restatement of
+    cost.py:88-99 on those ranges, 0 <= C <= E."""
+    _need(140)
+    g = _c4_graph()
+    eng = Q.Engine(N33)  # 128 GiB state + the 8 GiB table
+    try:
+        masks = np.ascontiguousarray(np.array(g.row_mask, dtype=np.uint64))
+        eng.call("qaoa_set_graph", N33, masks.ctypes.data_as(_lib._u64p), g.tot_edge, 0)
+        eng.call("qaoa_build_cut_table")
+        size = 1 << N33
+        chunk = 1 << 27
+        total = 0
+        buf = np.empty(chunk, dtype=np.int64)
+        cmin, cmax = 1 << 30, -1
+        for off in range(0, size, chunk):
+            eng.call("qaoa_read_cut_table", off, chunk, buf.ctypes.data_as(_lib._i64p))
+            total += int(buf.sum())
+            cmin, cmax = min(cmin, int(buf.min())), max(cmax, int(buf.max()))
+        assert total == g.tot_edge * (1 << (N33 - 1))
+        assert cmin == 0 and cmax <= g.tot_edge
+        for off in _sample_offsets(N33)[::8]:
+            lo = np.empty(BLOCK, dtype=np.int64)
+            hi = np.empty(BLOCK, dtype=np.int64)
+            eng.call("qaoa_read_cut_table", off, BLOCK, lo.ctypes.data_as(_lib._i64p))
+            eng.call("qaoa_read_cut_table", size - off - BLOCK, BLOCK, hi.ctypes.data_as(_lib._i64p))
+            assert np.array_equal(lo, hi[::-1])
+            xs = np.arange(off, off + BLOCK, dtype=np.uint64)
+            assert np.array_equal(lo, _cut_counts_numpy(g.row_mask, xs))
+    finally:
+        eng.close()
+
+
+def test_c4_sixteen_virtual_shards(c4_fast_p4):
+    """N=33 over 16 virtual shards of 2^29 (fused path: segmented shard runs +
+    in-place exchange kernel): x_hi = rank << 29 reaches node bit 32.  <C> and
+    the true amplitudes at the C4 sample indices equal the unsharded run's."""
+    from paper_2312_03019_b200.sharded import (
+        CudaShard,
+        PeerExchanger,
+        sharded_expectation,
+        simulate_sharded_fused,
+    )
+    import torch
+
+    _need(130)
+    g = _c4_graph()
+    pr = Q.params_from_seed(4, 0)
+    fs, fe, _ = c4_fast_p4
+    gbits = 4
+    shards = [CudaShard(N33 - gbits, r) for r in range(1 << gbits)]
+    try:
+        layout = simulate_sharded_fused(g, pr, shards, PeerExchanger(shards), gbits, expect=True)
+        e = sharded_expectation(shards)
+        cmask = shards[0].get_cmask()
+        idx = np.concatenate([np.arange(o, o + BLOCK, dtype=np.uint64)
+                              for o in _sample_offsets(N33)])
+        phys = layout.logical_to_physical(idx) ^ np.uint64(cmask)
+        nl = layout.n_local
+        rank = (phys >> np.uint64(nl)).astype(np.int64)
+        local = (phys & np.uint64((1 << nl) - 1)).astype(np.int64)
+        got = np.empty(idx.size, dtype=np.complex128)
+        for r, sh in enumerate(shards):
+            sel = np.nonzero(rank == r)[0]
+            if sel.size:
+                t = sh.tensor()
+                got[sel] = t[torch.as_tensor(local[sel], device=t.device)].cpu().numpy()
+    finally:
+        for sh in shards:
+            sh.close()
+    assert e == pytest.approx(fe, rel=EXP_RTOL)
+    assert np.max(np.abs(got - fs)) <= AMP_TOL
+
+
+# ---- config C3 against the oracle port on the host --------------------------
+def test_c3_n30_p10_vs_oracle_port(oracle):
+    """u3r N=30 p=10 (the bench's headline config): the oracle port (the
+    reference's arithmetic restated in C, pinned to the reference's own
+    outputs) runs the whole circuit on the host's threads (~2 min); the GPU's
+    exact schedule equals it bit for bit over all 2^30 amplitudes, the fast
+    schedule within 1e-12, <C> within 1e-10."""
+    import os
+
+    import psutil
+
+    if psutil.virtual_memory().available < 40 * 2**30:
+        pytest.skip("needs 40 GiB of host memory for the 16 GiB oracle state")
+    n = 30
+    g = Q.random_regular_graph(n, 3, seed=0)
+    pr = Q.params_from_seed(10, 0)
+    threads = len(os.sched_getaffinity(0))
+    ref = oracle.simulate(n, g.row_mask, g.tot_edge, pr.gamma, pr.beta, threads=threads)
+    eref = oracle.expectation(n, g.row_mask, ref, threads=threads)
+    chunk = 1 << 26
+    for exact in (True, False):
+        s = Q.simulate(g, pr, "bitwise", exact=exact, max_qubits=n)
+        try:
+            e = Q.expectation(g, s)
+            eng = s.engine()
+            worst = 0.0
+            for off in range(0, 1 << n, chunk):
+                got = eng.read(off, chunk)
+                if exact:
+                    assert np.array_equal(got, ref[off:off + chunk]), off
+                else:
+                    worst = max(worst, float(np.max(np.abs(got - ref[off:off + chunk]))))
+        finally:
+            s.engine().close()
+        assert worst <= AMP_TOL
+        assert e == pytest.approx(eref, rel=EXP_RTOL)
