@@ -19,9 +19,9 @@ chunk exchange per level).  ``--replicas`` instead runs one full state per rank
 (weak scaling).  Device time is the max over ranks.
 
 ``--impl reference`` times the CPU oracle (oracle/, a C restatement of the
-reference's algorithm, bit-exact with it) on all host threads: each step is one
-level of the same graph family at N=28 (a bounded sample; the rate is converted
-to N=30 levels/s by the (N+1) 2^N amplitude-update count).
+reference's algorithm, bit-exact with it) on all host threads at the same
+config: each step is one level of the same N=30 p=10 circuit (~12 s on 16
+threads), plus the cut-table build, expectation and a 1-thread sample.
 """
 
 from __future__ import annotations
@@ -57,7 +57,6 @@ def l2_note(state_bytes, shards=1):
 
 
 UNIT = "layers/s"
-REF_SAMPLE_N = 28
 
 
 def dist_env():
@@ -171,56 +170,157 @@ class ClockSampler:
         return out
 
 
-def cpu_reference_rate(threads: int, levels: int = 1):
-    """Oracle (C port of the reference, bit-exact with it) on the host: amplitude
-    updates per second over `levels` levels of u3r N=28 (init + cost + mixer)."""
+def ref_graph_edges(n: int, graph: str):
+    """The bench graph restated with the oracle's generators (the GPU box has no
+    /root/reference): u3r seed 0 (graph.py:170-205; odd N: u3r(N-1) plus an
+    isolated node) or ER(0.5) seed 0 (test_acceptance.py:46-57 pattern)."""
     from oracle import oracle as O
 
-    n = REF_SAMPLE_N
-    edges = O.random_regular_edges(n, 3, 0)
-    rm = O.row_masks(n, edges)
-    gm, bt = O.params_from_seed(10, 0)
-    t0 = time.perf_counter()
-    amps = O.simulate(n, rm, len(edges), gm[:levels], bt[:levels], threads=threads)
-    dt = time.perf_counter() - t0
-    del amps
-    return levels * (n + 1) * (1 << n) / dt, dt
+    if graph == "er":
+        rng = np.random.default_rng(0)
+        return [(i, j) for i in range(n) for j in range(i + 1, n) if rng.random() < 0.5]
+    return O.random_regular_edges(n - (n % 2), 3, 0)
+
+
+class RefLevels:
+    """The reference's CPU path (oracle port: cost.py:162-176 + circuit.py:89-94,
+    bit-exact with the reference) on the host, one QAOA level per call, cycling
+    through the p levels of params_from_seed(p, 0); level 0 includes the
+    launch-control init (circuit.py:42-48)."""
+
+    def __init__(self, n: int, p: int, graph: str, threads: int):
+        from oracle import oracle as O
+
+        self.O, self.n, self.p, self.threads = O, n, p, threads
+        edges = ref_graph_edges(n, graph)
+        self.rm = O.row_masks(n, edges)
+        self.E = len(edges)
+        self.gm, self.bt = O.params_from_seed(p, 0)
+        self.amps = np.empty(1 << n, dtype=np.complex128)
+        self.level = 0
+
+    def step(self) -> float:
+        O, t0 = self.O, time.perf_counter()
+        if self.level == 0:
+            O.lib().orc_init_uniform(self.n, O._ptr(self.amps, O._f64p), self.threads)
+        O.apply_cost(self.amps, self.n, self.rm, self.E, self.gm[self.level], threads=self.threads)
+        O.apply_mixer(self.amps, self.n, self.bt[self.level], threads=self.threads)
+        self.level = (self.level + 1) % self.p
+        return time.perf_counter() - t0
+
+    def cut_table_s(self) -> float:
+        t0 = time.perf_counter()
+        ct = self.O.cut_counts(self.n, self.rm, threads=self.threads)
+        dt = time.perf_counter() - t0
+        del ct
+        return dt
+
+    def expectation(self) -> tuple[float, float]:
+        t0 = time.perf_counter()
+        e = self.O.expectation(self.n, self.rm, self.amps, threads=self.threads)
+        return e, time.perf_counter() - t0
+
+
+def cpu_reference_level(n: int, p: int, graph: str, threads: int):
+    """One level (init + cost + mixer) of the bench's own config on the host:
+    the GPU line's bounded cpu_baseline sample (~12 s at N=30 on 16 threads)."""
+    r = RefLevels(n, p, graph, threads)
+    dt = r.step()
+    del r
+    return (n + 1) * (1 << n) / dt, dt
+
+
+def single_thread_sample(n: int, graph: str, n_sample: int = 24):
+    """T=1 beside T=all: one level at a bounded size."""
+    n_sample = min(n, n_sample)
+    r = RefLevels(n_sample, 1, graph, 1)
+    dt = r.step()
+    return {"threads": 1, "sample": f"1 level of the same graph family at N={n_sample}",
+            "level_s": dt, "amp_updates_per_s": (n_sample + 1) * (1 << n_sample) / dt,
+            "layers_per_s_at_N": (n_sample + 1) * (1 << n_sample) / dt / ((n + 1) * (1 << n))}
 
 
 def run_reference(args, rank: int, world: int):
+    """The reference arm: the reference's CPU path (oracle port) at the GPU
+    line's own config (N, p, graph, angles), one QAOA level per step, all host
+    threads.  Also times the cut-table build (cost.py:88-99, pre-warmed by the
+    reference before its layers) and expectation (circuit.py:116-121) apart,
+    and a single-thread sample."""
     if rank != 0:
         return 0
     from oracle import oracle as O
 
     O.lib()
+    t_start = time.perf_counter()
     threads = len(os.sched_getaffinity(0))
     n, p = args.n, args.p
     per_level = (n + 1) * (1 << n)
+    ref = RefLevels(n, p, args.graph, threads)
+    table_s = ref.cut_table_s()
     for _ in range(args.warmup):
-        cpu_reference_rate(threads)
-    rates, secs = [], 0.0
-    for _ in range(args.steps):
-        r, dt = cpu_reference_rate(threads)
-        rates.append(r)
-        secs += dt
-    rate = statistics.median(rates)
-    layers = rate / per_level
+        ref.step()
+    times = [ref.step() for _ in range(args.steps)]
+    total = sum(times)
+    e_val, expect_s = ref.expectation()
+    complete = (args.warmup + args.steps) % p == 0
+    t1 = single_thread_sample(n, args.graph)
+    layers = args.steps / total
+    wall = time.perf_counter() - t_start
     line = {
         "impl": "reference", "metric": METRIC, "value": layers, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * p / layers, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": workload_name(args),
                    "n_qubits": n, "p": p, "graph": args.graph,
+                   "schedule": "reference (cost layer + n RX per level, increasing qubit order)",
+                   "parallelism": "host CPU, OpenMP",
                    "l2": l2_note(16 << n)},
-        "amp_updates_per_s": rate,
+        "step": "one QAOA level of the config's p-level circuit (levels cycle 0..p-1; "
+                "level 0 includes the launch-control init)",
+        "amp_updates_per_s": layers * per_level,
+        "level_s": {"median": statistics.median(times), "min": min(times), "max": max(times)},
+        "cut_table_build_s": table_s,
+        "expectation_s": expect_s,
+        "expectation": e_val if complete else None,
+        "single_thread": t1,
         "cpu_baseline": {"value": layers, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"1 level (init+cost+mixer) of u3r N={REF_SAMPLE_N} per step, "
-                                   f"rate scaled to N={n} by (N+1)2^N amplitude updates"},
+                         "sample": f"{args.steps} timed levels of the config itself "
+                                   f"(N={n}, p={p}, {args.graph}) after {args.warmup} warm-up levels"},
         "e2e": {"value": layers, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "consistency": {"timed_s": total, "wall_s": wall},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def p1_closed_form(n: int, edges, gamma: float, beta: float) -> float:
+    """<C> of a p=1 circuit on any unweighted graph, edge by edge (Wang, Hadfield,
+    Jiang, Rieffel 2018, mapped to the reference's convention).
+    The check for states no CPU can hold (N=36 over 8 GPUs)."""
+    adj = [set() for _ in range(n)]
+    for i, j in edges:
+        adj[i].add(j)
+        adj[j].add(i)
+    s2b, sb2 = math.sin(2 * beta), math.sin(beta) ** 2
+    cg, c2g, sg = math.cos(gamma), math.cos(2 * gamma), math.sin(gamma)
+    total = 0.0
+    for u, v in edges:
+        du, dv, lam = len(adj[u]) - 1, len(adj[v]) - 1, len(adj[u] & adj[v])
+        total += 0.5 + 0.25 * s2b * sg * (cg ** du + cg ** dv) \
+            - 0.25 * sb2 * cg ** (du + dv - 2 * lam) * (1 - c2g ** lam)
+    return total
+
+
+def closed_form_check(g, params, value):
+    """p=1 runs: <C> against the closed form; raises past the 1e-10 contract."""
+    if params.p != 1:
+        return None
+    cf = p1_closed_form(g.n, [(i, j) for i, j, _ in g.edges], params.gamma[0], params.beta[0])
+    rel = abs(value - cf) / abs(cf)
+    if rel > 1e-10:
+        raise SystemExit(f"<C> = {value!r} differs from the p=1 closed form {cf!r} (rel {rel:.2e})")
+    return {"value": cf, "rel_err": rel}
 
 
 def make_graph(Q, args):
@@ -258,8 +358,11 @@ def run_sharded(args, rank: int, world: int, local: int):
         local = 0
     dist = init_dist(world, local, args.dist_backend)
     torch.cuda.set_device(local)
-    n, p = args.n, args.p
     gbits = world.bit_length() - 1
+    # strong: the --qubits state over the G GPUs; weak: 2^qubits amplitudes per GPU
+    # (N = qubits + log2 G: 33@1 -> 36@8 at 128 GiB per GPU)
+    n, p = (args.n + gbits if args.scaling == "weak" else args.n), args.p
+    args.n = n
     g = make_graph(Q, args)
     params = Q.params_from_seed(p, 0)
     fused = args.exchange == "ipc"
@@ -286,7 +389,8 @@ def run_sharded(args, rank: int, world: int, local: int):
                           stream=torch.cuda.current_stream(local).cuda_stream)
     if exch is None:
         exch = DistExchanger(shard, rank, world)
-
+    if hasattr(exch, "timing"):
+        exch.timing = True  # CUDA events around every exchange kernel launch
     def step():
         if fused:
             simulate_sharded_fused(g, params, [shard], exch, gbits, exact=args.exact, expect=True)
@@ -302,6 +406,9 @@ def run_sharded(args, rank: int, world: int, local: int):
         val = step()
     dist.barrier()
     torch.cuda.synchronize(local)
+    if hasattr(exch, "exchange_ms"):
+        exch.collect()
+        exch.exchange_ms.clear()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
     step_bytes = 0.0
@@ -318,6 +425,15 @@ def run_sharded(args, rank: int, world: int, local: int):
         torch.cuda.synchronize(local)
         wall_s = time.perf_counter() - t0
     dev_ms = start.elapsed_time(stop)
+    xms = None
+    if getattr(exch, "exchange_ms", None) is not None:
+        exch.collect()
+        if exch.exchange_ms:
+            xms = statistics.mean(exch.exchange_ms)
+    tx = torch.tensor([xms if xms is not None else -1.0], dtype=torch.float64,
+                      device="cpu" if args.dist_backend == "gloo" else f"cuda:{local}")
+    tdist.all_reduce(tx, op=tdist.ReduceOp.MAX)
+    xms = float(tx.item()) if tx.item() > 0 else None
     tw = torch.tensor([wall_s], dtype=torch.float64,
                       device="cpu" if args.dist_backend == "gloo" else f"cuda:{local}")
     tdist.all_reduce(tw, op=tdist.ReduceOp.MAX)
@@ -335,7 +451,7 @@ def run_sharded(args, rank: int, world: int, local: int):
         line = {
             "metric": METRIC, "value": layers, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "c128",
             "data": "synthetic",
             "config": {"workload": workload_name(args),
                        "n_qubits": n, "p": p, "graph": args.graph,
@@ -349,9 +465,19 @@ def run_sharded(args, rank: int, world: int, local: int):
             "exchange_fallback": fallback,
             "nvlink": {"bytes_per_level_per_rank_per_direction": xbytes,
                        "peak_GBps_per_direction": 770.0,
+                       "peak_kind": "measured 8-rank bus bandwidth (B200_PROFILING.md); "
+                                    "900 GB/s nominal NVLink 5",
+                       # per exchange: (G-1)/G of this rank's slice of 16 B x 2^n_local
+                       # crosses NVLink in each direction; kernel time from CUDA
+                       # events around every exchange launch, max over ranks
+                       "exchange_ms": xms,
+                       "achieved_GBps_per_direction": (xbytes / (xms * 1e-3) / 1e9) if xms else None,
+                       "frac": (xbytes / (xms * 1e-3) / 1e9 / 770.0) if xms else None,
+                       "exchanges_per_step": p,
                        # step-level: exchange bytes over the whole step time (the
                        # exchange overlaps the sweeps, so this is a lower bound)
                        "achieved_GBps_step_level": xbytes * p / step_s / 1e9},
+            "closed_form_p1": closed_form_check(g, params, val),
             # step-level roofline: a rank's sweep bytes over the whole step,
             # exchange and peer waits included (no per-kernel split here: the
             # pipelined sweeps run as tile ranges interleaved with the exchange)
@@ -394,8 +520,8 @@ def run_ours(args, rank: int, world: int, local: int):
     tables, cs, ss = Q.level_arrays(g, params)
     stream = torch.cuda.Stream(device)
     eng = Q.Engine(n, device, stream=stream.cuda_stream)
-    if n > 30:
-        args.e2e_steps = min(args.e2e_steps, 2)
+    if args.e2e_steps is None:  # same step count as the device-timed loop
+        args.e2e_steps = args.steps
     eng.ensure_graph(g)
     flags = _lib.RUN_EXPECTATION | _lib.RUN_TIMING | (_lib.RUN_EXACT if args.exact else 0)
     L = _lib.load()
@@ -476,9 +602,12 @@ def run_ours(args, rank: int, world: int, local: int):
         torch.cuda.synchronize(device)
         ms = ev0.elapsed_time(ev1)
         bpe = 1 if g.tot_edge <= 255 else 2
-        cut_table = {"ms": ms, "states_per_s": (1 << n) / (ms * 1e-3),
-                     "bytes_written": bpe << n, "GBps": (bpe << n) / (ms * 1e-3) / 1e9,
-                     "dtype": "uint8" if bpe == 1 else "uint16"}
+        gbps = (bpe << n) / (ms * 1e-3) / 1e9
+        cut_table = {"kernel": "qb::cut_table_warp_kernel (K1, SURVEY 8a a3: cost.py:88-99)",
+                     "ms": ms, "states_per_s": (1 << n) / (ms * 1e-3),
+                     "bytes_written": bpe << n, "GBps": gbps, "dtype": "uint8" if bpe == 1 else "uint16",
+                     # K1's roofline is its table write, w_C 2^N bytes
+                     "roofline_frac": gbps / peak}
         eng.call("qaoa_free_cut_table")
 
     # ---- end to end through the public API: host inputs -> <C> on the host ----
@@ -503,9 +632,8 @@ def run_ours(args, rank: int, world: int, local: int):
         e2e = {"value": world * p * args.e2e_steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8,
                "api": "paper_2312_03019_b200.simulate + expectation",
-               # a separate timed loop (wall clock, host inputs): the sweeps run at
-               # the board power limit, so it can land a little above `value`
-               # (whose loop also records per-sweep events) -- same kernels
+               # a separate loop of the same K steps (wall clock, host inputs,
+               # every step synchronous): the same kernels as `value`
                "steps": args.e2e_steps}
         assert abs(val - expect_val) <= 1e-10 * abs(expect_val)
 
@@ -513,10 +641,11 @@ def run_ours(args, rank: int, world: int, local: int):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = len(os.sched_getaffinity(0))
-            rate, dt = cpu_reference_rate(threads)
+            rate, dt = cpu_reference_level(n, p, args.graph, threads)
             cpu = {"value": rate / per_level, "unit": UNIT, "cores": threads, "kind": "port",
-                   "sample": f"1 level of u3r N={REF_SAMPLE_N} on the oracle (C port, "
-                             f"{threads} OpenMP threads, {dt:.1f} s), scaled to N={n} levels/s",
+                   "sample": f"level 1 (init + cost + mixer) of this config (N={n}, {args.graph}) "
+                             f"on the oracle (C port of the reference path, {threads} OpenMP "
+                             f"threads, {dt:.1f} s)",
                    "amp_updates_per_s": rate}
         except Exception as exc:  # the CPU baseline must never sink the GPU line
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
@@ -534,6 +663,7 @@ def run_ours(args, rank: int, world: int, local: int):
                        "l2": l2_note(16 << n)},
             "amp_updates_per_s": layers_per_s * per_level,
             "expectation": expect_val,
+            "closed_form_p1": closed_form_check(g, params, expect_val),
             "cut_table_build": cut_table,
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -565,9 +695,11 @@ def main():
                          "(configs[3], the dense N=33 cut-table stress case)")
     ap.add_argument("--levels", dest="p", type=int, default=10)
     ap.add_argument("--exact", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="end-to-end loop steps (default: --steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cut-table", action="store_true", help="also time the K1 cut-table builder")
+    ap.add_argument("--no-cut-table", dest="cut_table", action="store_false",
+                    help="skip timing the K1 cut-table builder")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo = test mode (exchanges staged through host memory)")
     ap.add_argument("--share-device", action="store_true",
@@ -579,6 +711,10 @@ def main():
     ap.add_argument("--chunks", type=int, default=4,
                     help="sharded ipc runs: pipeline each exchange with the sweeps around it "
                          "in this many chunks (1 = no overlap)")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="N>1: strong = the --qubits state sharded over the GPUs; weak = "
+                         "2^qubits amplitudes per GPU (N = qubits + log2 GPUs), e.g. "
+                         "--qubits 33 --scaling weak: 33@1 .. 36@8")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: one full state per rank (weak scaling) instead of sharding")
     args = ap.parse_args()

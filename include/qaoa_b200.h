@@ -105,6 +105,24 @@ QAOA_API int qaoa_apply_cost(qaoa_ctx* ctx, const double* phase_table);
  * s = sin(theta/2).  Bit-exact (products rounded separately). */
 QAOA_API int qaoa_apply_rx(qaoa_ctx* ctx, int qubit, double c, double s);
 
+/* Gate-level baseline (the reference's default backend "baseline" and
+ * init_state(launch_control=False), circuit.py:57-62,76-80).
+ * qaoa_init_basis: |index> (init_zero_state, state.py:66-72, index 0); resets
+ * the complement mask.  qaoa_apply_h: Hadamard (apply_h, state.py:91-107),
+ * (a +- b) * (1/sqrt 2) rounded as the reference does.  qaoa_apply_rzz: RZZ
+ * (apply_rzz, state.py:131-149) with phases = {e_same.re, e_same.im, e_diff.re,
+ * e_diff.im} formed by the caller as the reference forms them
+ * (np.exp(-+0.5j*theta)); FMA-form complex multiply.  All bit-exact. */
+QAOA_API int qaoa_init_basis(qaoa_ctx* ctx, uint64_t index);
+QAOA_API int qaoa_apply_h(qaoa_ctx* ctx, int qubit);
+QAOA_API int qaoa_apply_rzz(qaoa_ctx* ctx, int q1, int q2, const double* phases);
+
+/* Per-index edge sums over the edge list of qaoa_set_weights, in edge order,
+ * for true indices x_hi | [offset, offset + count): kind 0 = signed rotation
+ * totals (CompressedCostPlan.rotation_totals, cost.py:77-86), kind 1 = cut
+ * values (cut_values_array, graph.py:144-151).  Bit-identical float64. */
+QAOA_API int qaoa_edge_values(qaoa_ctx* ctx, int kind, uint64_t offset, uint64_t count, double* out);
+
 /* Mixer layer (apply_mixer_layer, circuit.py:89-94): RX on every local qubit in
  * increasing order, c = cos(-beta/2), s = sin(-beta/2).  Bit-exact. */
 QAOA_API int qaoa_apply_mixer(qaoa_ctx* ctx, double c, double s);

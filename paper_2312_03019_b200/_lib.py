@@ -60,6 +60,10 @@ SIGNATURES = {
     "qaoa_apply_cost": (_c_int, [_vp, _dp]),
     "qaoa_apply_rx": (_c_int, [_vp, _c_int, _c_dbl, _c_dbl]),
     "qaoa_apply_mixer": (_c_int, [_vp, _c_dbl, _c_dbl]),
+    "qaoa_init_basis": (_c_int, [_vp, _u64]),
+    "qaoa_apply_h": (_c_int, [_vp, _c_int]),
+    "qaoa_apply_rzz": (_c_int, [_vp, _c_int, _c_int, _dp]),
+    "qaoa_edge_values": (_c_int, [_vp, _c_int, _u64, _u64, _dp]),
     "qaoa_run_layers": (_c_int, [_vp, _c_int, _dp, _dp, _dp, _c_int]),
     "qaoa_apply_rx_range": (_c_int, [_vp, _c_int, _c_int, _c_dbl, _c_dbl, _c_int]),
     "qaoa_set_layout_swap": (_c_int, [_vp, _c_int]),

@@ -27,7 +27,11 @@ from .state import (
     DEFAULT_MAX_QUBITS,
     Engine,
     StateVector,
+    apply_h,
+    apply_rx,
+    apply_rzz,
     check_qubit_budget,
+    init_zero_state,
     write_counter,
 )
 
@@ -98,19 +102,38 @@ def init_uniform(n: int, max_qubits: int = DEFAULT_MAX_QUBITS) -> StateVector:
 
 def init_state(n: int, launch_control: bool = True, threads: int = 1,
                max_qubits: int = DEFAULT_MAX_QUBITS) -> StateVector:
-    """circuit.py:51-62.  Without launch control the reference applies n Hadamards
-    to |0..0>; the result is the uniform state up to rounding (<= 1e-16), which
-    the engine writes directly."""
-    return init_uniform(n, max_qubits)
+    """circuit.py:51-62: launch control writes the uniform state directly;
+    without it, |0..0> and one Hadamard per qubit in increasing order (the
+    reference's gate path, same rounding and write count)."""
+    if launch_control:
+        return init_uniform(n, max_qubits)
+    s = init_zero_state(n, max_qubits)
+    for q in range(n):
+        apply_h(s, q, threads=threads)
+    return s
+
+
+def _init_on(eng: Engine, n: int) -> None:
+    """|0..0> plus n Hadamards on an existing engine (launch_control=False)."""
+    eng.call("qaoa_init_basis", 0)
+    for q in range(n):
+        eng.call("qaoa_apply_h", q)
+    write_counter.add((n + 1) << n)
 
 
 def apply_cost_layer(s: StateVector, g: Graph, gamma: float, backend: str = "baseline",
                      threads: int = 1, batch_width: int | None = None,
                      use_table_popcount: bool = False) -> StateVector:
-    """One cost layer, one device pass (circuit.py:65-86)."""
+    """One cost layer (circuit.py:65-86): "baseline" = one RZZ(w gamma) pass per
+    edge in the graph's edge order (state.py:131-149); the other backends one
+    compressed device pass."""
     validate_backend(backend, g)
     from .cost import apply_cost_batched, apply_cost_bitwise, apply_cost_compressed
 
+    if backend == "baseline":
+        for i, j, w in g.edges:
+            apply_rzz(s, i, j, w * gamma, threads=threads)
+        return s
     plan = plan_for(g)
     if not g.is_unweighted:
         return apply_cost_compressed(s, plan, gamma, threads)
@@ -145,8 +168,10 @@ def simulate(
     store_state: bool = True,
 ) -> StateVector:
     """Run the p-level circuit on the GPU and return the device-resident state
-    (circuit.py:97-113).  All three backend names select the fused engine (they
-    are numerically equivalent on unweighted graphs: test_acceptance.py:60-79).
+    (circuit.py:97-113).  backend="baseline" (the reference's default) is the
+    gate-level path: one device pass per RZZ (edge) and per RX (qubit), bit for
+    bit the reference's baseline; "bitwise" / "compressed" run the fused engine.
+    launch_control=False starts from |0..0> plus n Hadamards (circuit.py:57-62).
 
     Extra keyword-only knobs: ``exact`` (bit-exact reference schedule),
     ``device``, ``fuse_expectation`` (accumulate <C> in the last sweep) and
@@ -163,6 +188,8 @@ def simulate(
     if batch_width is not None and batch_width not in (1, 2, 4, 8):
         raise ValueError(f"batch width must be 1, 2, 4, or 8, got {batch_width}")
     check_qubit_budget(g.n, max_qubits)
+    if backend == "baseline":
+        return _simulate_gates(g, params, launch_control, threads, max_qubits, state)
     if state is not None and state.n == g.n:
         eng = state._eng if state._eng is not None else Engine(g.n, device)
         state._eng, state._host, state._where = eng, None, "device"
@@ -171,6 +198,10 @@ def simulate(
         eng = Engine(g.n, device)
         s = StateVector(g.n, engine=eng)
     eng.ensure_graph(g)
+    from_state = 0
+    if not launch_control:
+        _init_on(eng, g.n)
+        from_state = _lib.RUN_FROM_STATE
     if not g.is_unweighted:
         eng.ensure_weights(g)
         if not exact and g.n >= 12 and params.p > 0:
@@ -178,27 +209,50 @@ def simulate(
             gm = np.ascontiguousarray(np.array(params.gamma, dtype=np.float64))
             cs = np.array([rx_coefficients(b)[0] for b in params.beta], dtype=np.float64)
             ss = np.array([rx_coefficients(b)[1] for b in params.beta], dtype=np.float64)
-            wflags = _lib.RUN_EXPECTATION if fuse_expectation else 0
+            wflags = (_lib.RUN_EXPECTATION if fuse_expectation else 0) | from_state
             if not store_state and fuse_expectation:
                 wflags |= _lib.RUN_EXPECT_ONLY
             eng.call("qaoa_run_layers_weighted", params.p, _lib.dptr(gm), _lib.dptr(cs),
                      _lib.dptr(ss), wflags)
         else:
             # reference order and rounding: edge-order totals, exact mixer sweeps
-            eng.call("qaoa_init_uniform")
+            if launch_control:
+                eng.call("qaoa_init_uniform")
             for gamma, beta in zip(params.gamma, params.beta):
                 eng.call("qaoa_apply_cost_weighted", float(gamma))
                 c, sn = rx_coefficients(beta)
                 eng.call("qaoa_apply_mixer", c, sn)
-        write_counter.add((1 << g.n) * (1 + params.p * (g.n + 1)))
+        write_counter.add((1 << g.n) * (int(launch_control) + params.p * (g.n + 1)))
         return s
     tables, cs, ss = level_arrays(g, params)
-    flags = (_lib.RUN_EXACT if exact else 0) | (_lib.RUN_EXPECTATION if fuse_expectation else 0)
+    flags = (_lib.RUN_EXACT if exact else 0) | (_lib.RUN_EXPECTATION if fuse_expectation else 0) \
+        | from_state
     if not store_state and fuse_expectation:
         flags |= _lib.RUN_EXPECT_ONLY
     eng.call("qaoa_run_layers", params.p, _lib.dptr(tables.view(np.float64)), _lib.dptr(cs),
              _lib.dptr(ss), flags)
-    write_counter.add((1 << g.n) * (1 + params.p * (g.n + 1)))
+    write_counter.add((1 << g.n) * (int(launch_control) + params.p * (g.n + 1)))
+    return s
+
+
+def _simulate_gates(g: Graph, params: QaoaParams, launch_control: bool, threads: int,
+                    max_qubits: int, state: StateVector | None) -> StateVector:
+    """The reference's gate-level circuit on the GPU (backend "baseline",
+    circuit.py:108-113): init_state, then per level one RZZ pass per edge and
+    one RX pass per qubit -- the comparison baseline of run_compare
+    (bench.py:184-243), bit-identical to the reference."""
+    if state is not None and state.n == g.n and launch_control:
+        eng = state._eng if state._eng is not None else Engine(g.n)
+        state._eng, state._host, state._where = eng, None, "device"
+        eng.call("qaoa_init_uniform")
+        write_counter.add(1 << g.n)
+        s = state
+    else:
+        s = init_state(g.n, launch_control, threads, max_qubits)
+    for gamma, beta in zip(params.gamma, params.beta):
+        apply_cost_layer(s, g, gamma, "baseline", threads)
+        for q in range(g.n):
+            apply_rx(s, q, -beta, threads=threads)
     return s
 
 

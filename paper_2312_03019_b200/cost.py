@@ -64,6 +64,14 @@ class CompressedCostPlan:
         self.tot_edge = graph.tot_edge
         self.weights = tuple(w for _, _, w in graph.edges)
         self._cut_counts: np.ndarray | None = None
+        self._rotation_totals: np.ndarray | None = None
+
+    def rotation_totals(self) -> np.ndarray:
+        """Signed rotation total sum_e w_e (1 - 2 [x_i != x_j]) per basis index,
+        float64, accumulated in edge order on the GPU (cost.py:77-86; bit-identical)."""
+        if self._rotation_totals is None:
+            self._rotation_totals = edge_values(self.graph, 0)
+        return self._rotation_totals
 
     def _require_unweighted(self) -> None:
         if not self.graph.is_unweighted:
@@ -90,6 +98,20 @@ def build_cut_table(g: Graph, device: int = 0) -> np.ndarray:
         eng.call("qaoa_build_cut_table")
         out = np.empty(1 << g.n, dtype=np.int64)
         eng.call("qaoa_read_cut_table", 0, out.size, out.ctypes.data_as(_lib._i64p))
+        return out
+    finally:
+        eng.close()
+
+
+def edge_values(g: Graph, kind: int, device: int = 0) -> np.ndarray:
+    """Per-index float64 edge sums in edge order, computed on the GPU
+    (qaoa_edge_values): kind 0 = rotation totals (cost.py:77-86), kind 1 = cut
+    values (graph.py:144-151)."""
+    eng = Engine(g.n, device)
+    try:
+        eng.ensure_weights(g)
+        out = np.empty(1 << g.n, dtype=np.float64)
+        eng.call("qaoa_edge_values", int(kind), 0, out.size, _lib.dptr(out))
         return out
     finally:
         eng.close()

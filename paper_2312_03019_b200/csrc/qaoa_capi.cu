@@ -479,7 +479,7 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
   R.p = p;
   const int n = c->n;
   const int n_total = c->g.n_nodes;
-  const double u = sqrt(1.0 / (double)(1ull << n_total));
+  const double u = sqrt(ldexp(1.0, -n_total));  // 1/2^n exactly for n <= 64
   const uint64_t size = 1ull << n;
   c->expect_valid = false;
   c->last_launches = 0;
@@ -615,7 +615,7 @@ int launch_plan_sweep(qaoa_ctx* c, int i, int64_t lo, int64_t cnt) {
   RunState& R = c->run;
   const uint64_t size = 1ull << c->n;
   const int te = c->g.tot_edge + 1;
-  const double u = sqrt(1.0 / (double)(1ull << c->g.n_nodes));
+  const double u = sqrt(ldexp(1.0, -c->g.n_nodes));
   const SweepPlan& sp = R.plan[i];
   // swapped layout: sets 1 and last trade physical positions
   const int ns = (int)R.sets.size();
@@ -834,7 +834,7 @@ int qaoa_init_uniform(qaoa_ctx* c) {
   if (rc) return rc;
   c->state_stale = false;
   const int n_total = c->has_graph ? c->g.n_nodes : c->n;
-  const double u = sqrt(1.0 / (double)(1ull << n_total));
+  const double u = sqrt(ldexp(1.0, -n_total));  // 1/2^n exactly for n <= 64
   CUDA_TRY(launch_fill(c->amps, 1ull << c->n, make_double2(u, 0.0), c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   c->expect_valid = false;
@@ -966,6 +966,79 @@ int qaoa_apply_rx(qaoa_ctx* c, int qubit, double cs, double sn) {
   return QAOA_OK;
 }
 
+// ---- gate-level baseline (state.py:66-149) ----------------------------------
+int qaoa_init_basis(qaoa_ctx* c, uint64_t index) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (c->n < 64 && index >= (1ull << c->n)) return fail(QAOA_E_RANGE, "basis index out of range");
+  c->state_stale = false;
+  CUDA_TRY(launch_basis(c->amps, 1ull << c->n, index, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->expect_valid = false;
+  c->g.cmask = 0;
+  return QAOA_OK;
+}
+
+int qaoa_apply_h(qaoa_ctx* c, int qubit) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if ((rc = require_stored(c))) return rc;
+  if (qubit < 0 || qubit >= c->n) {
+    char buf[96];
+    snprintf(buf, sizeof buf, "qubit %d out of range for n=%d", qubit, c->n);
+    return fail(QAOA_E_RANGE, buf);
+  }
+  CUDA_TRY(launch_h_gate(c->amps, c->n, qubit, (int)((c->g.cmask >> qubit) & 1ull), c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->expect_valid = false;
+  return QAOA_OK;
+}
+
+int qaoa_apply_rzz(qaoa_ctx* c, int q1, int q2, const double* phases) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if ((rc = require_stored(c))) return rc;
+  if (!phases) return fail(QAOA_E_INVALID, "null phases");
+  if (q1 == q2) return fail(QAOA_E_INVALID, "RZZ needs two distinct qubits");
+  for (int q : {q1, q2})
+    if (q < 0 || q >= c->n) {
+      char buf[96];
+      snprintf(buf, sizeof buf, "qubit %d out of range for n=%d", q, c->n);
+      return fail(QAOA_E_RANGE, buf);
+    }
+  const uint64_t xbase = c->g.cmask & ((c->n >= 64) ? ~0ull : ((1ull << c->n) - 1ull));
+  CUDA_TRY(launch_rzz_gate(c->amps, 1ull << c->n, xbase, q1, q2, make_double2(phases[0], phases[1]),
+                           make_double2(phases[2], phases[3]), c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->expect_valid = false;
+  return QAOA_OK;
+}
+
+int qaoa_edge_values(qaoa_ctx* c, int kind, uint64_t offset, uint64_t count, double* out) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (kind != 0 && kind != 1) return fail(QAOA_E_INVALID, "kind must be 0 (rotation totals) or 1 (cut values)");
+  if (c->n_wedges < 0) return fail(QAOA_E_STATE, "no weighted edge list set");
+  if (offset > (1ull << c->n) || count > (1ull << c->n) - offset)
+    return fail(QAOA_E_RANGE, "index range out of bounds");
+  if (count && !out) return fail(QAOA_E_INVALID, "null destination");
+  const uint64_t chunk = std::min<uint64_t>(count, 1ull << 24);
+  double* d = nullptr;
+  if (chunk) CUDA_TRY(cudaMalloc(&d, chunk * sizeof(double)));
+  cudaError_t e = cudaSuccess;
+  for (uint64_t done = 0; done < count && e == cudaSuccess; done += chunk) {
+    const uint64_t k = std::min(chunk, count - done);
+    e = launch_edge_values(d, c->g.x_hi | (offset + done), k, c->d_ei, c->d_ej, c->d_w, c->n_wedges,
+                           kind, c->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(out + done, d, k * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  }
+  if (d) cudaFree(d);
+  CUDA_TRY(e);
+  return QAOA_OK;
+}
+
 static int run_exact_mixer_sweeps(qaoa_ctx* c, double cs, double sn) {
   // all sets, RX stage only, exact arithmetic and order
   const std::vector<SetDesc> sets = make_sets(c->n);
@@ -1062,7 +1135,7 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
   c->last_bytes = 0.0;
   c->times.clear();
   size_t ev = 0;
-  const double u = sqrt(1.0 / (double)(1ull << n_total));
+  const double u = sqrt(ldexp(1.0, -n_total));  // 1/2^n exactly for n <= 64
   const uint64_t size = 1ull << n;
 
   if (n < 12) {

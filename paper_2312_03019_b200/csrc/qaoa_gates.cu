@@ -113,6 +113,94 @@ cudaError_t launch_rx_gate(double2* amps, int n_local, int q, double c, double s
   return cudaGetLastError();
 }
 
+// ---- gate-level baseline (reference backend "baseline", launch_control=False)
+// Hadamard on qubit q (state.py:91-107): top = (a + b) * k, bot = (a - b) * k,
+// k = 1/sqrt(2) rounded once (state.py:22), every operation rounded separately.
+// `flip`: the stored state has qubit q complemented (fast-mode bookkeeping),
+// so the stored pair is (true b, true a): the same butterfly with the
+// outputs exchanged (a + b = b + a exactly).
+__global__ void h_gate_kernel(double2* __restrict__ amps, int n_local, int q, int flip,
+                              double k) {
+  const uint64_t half = 1ull << (n_local - 1);
+  const uint64_t stride = 1ull << q;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < half;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = ((i >> q) << (q + 1)) | (i & (stride - 1));
+    const double2 a = amps[i0], b = amps[i0 | stride];
+    const double2 top = make_double2(__dmul_rn(__dadd_rn(a.x, b.x), k), __dmul_rn(__dadd_rn(a.y, b.y), k));
+    const double2 bot = flip
+        ? make_double2(__dmul_rn(__dsub_rn(b.x, a.x), k), __dmul_rn(__dsub_rn(b.y, a.y), k))
+        : make_double2(__dmul_rn(__dsub_rn(a.x, b.x), k), __dmul_rn(__dsub_rn(a.y, b.y), k));
+    amps[i0] = flip ? bot : top;
+    amps[i0 | stride] = flip ? top : bot;
+  }
+}
+
+cudaError_t launch_h_gate(double2* amps, int n_local, int q, int flip, cudaStream_t s) {
+  const double k = 1.0 / sqrt(2.0);
+  h_gate_kernel<<<grid_for(1ull << (n_local - 1), 2), kBlock, 0, s>>>(amps, n_local, q, flip, k);
+  return cudaGetLastError();
+}
+
+// RZZ(theta) on qubits q1, q2 (state.py:131-149): amp *= (bit q1 != bit q2) ?
+// e_diff : e_same, the two phases formed on the host by numpy exactly as the
+// reference does; numpy's FMA-form complex multiply (cmul_np).  x = xbase ^ y
+// is the true index of stored element y (x_hi and the complement mask).
+__global__ void rzz_gate_kernel(double2* __restrict__ amps, uint64_t n, uint64_t xbase, int q1,
+                                int q2, double2 e_same, double2 e_diff) {
+  for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < n;
+       y += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = xbase ^ y;
+    const bool diff = ((x >> q1) ^ (x >> q2)) & 1ull;
+    amps[y] = cmul_np(amps[y], diff ? e_diff : e_same);
+  }
+}
+
+cudaError_t launch_rzz_gate(double2* amps, uint64_t n, uint64_t xbase, int q1, int q2,
+                            double2 e_same, double2 e_diff, cudaStream_t s) {
+  rzz_gate_kernel<<<grid_for(n, 4), kBlock, 0, s>>>(amps, n, xbase, q1, q2, e_same, e_diff);
+  return cudaGetLastError();
+}
+
+// |index>: zero everywhere, 1 at `index` (init_zero_state, state.py:66-72).
+__global__ void basis_kernel(double2* __restrict__ amps, uint64_t n, uint64_t index) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    __stcs(amps + i, make_double2(i == index ? 1.0 : 0.0, 0.0));
+}
+
+cudaError_t launch_basis(double2* amps, uint64_t n, uint64_t index, cudaStream_t s) {
+  basis_kernel<<<grid_for(n, 4), kBlock, 0, s>>>(amps, n, index);
+  return cudaGetLastError();
+}
+
+// Per-index edge sums in the reference's edge order for TRUE indices
+// x = first + i: kind 0 = rotation totals sum_e w_e (1 - 2 [x_i != x_j])
+// (CompressedCostPlan.rotation_totals, cost.py:77-86), kind 1 = cut values
+// sum_e w_e [x_i != x_j] (cut_values_array, graph.py:144-151); bit-identical.
+__global__ void edge_values_kernel(double* __restrict__ out, uint64_t first, uint64_t count,
+                                   const int* __restrict__ ei, const int* __restrict__ ej,
+                                   const double* __restrict__ w, int m, int kind) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = first + i;
+    double v = 0.0;
+    for (int e = 0; e < m; ++e) {
+      const uint64_t diff = ((x >> __ldg(ei + e)) ^ (x >> __ldg(ej + e))) & 1ull;
+      const double we = __ldg(w + e);
+      v = kind == 0 ? __dadd_rn(v, __dmul_rn(we, diff ? -1.0 : 1.0))
+                    : __dadd_rn(v, __dmul_rn(we, diff ? 1.0 : 0.0));
+    }
+    out[i] = v;
+  }
+}
+
+cudaError_t launch_edge_values(double* out, uint64_t first, uint64_t count, const int* ei,
+                               const int* ej, const double* w, int m, int kind, cudaStream_t s) {
+  edge_values_kernel<<<grid_for(count, 1), kBlock, 0, s>>>(out, first, count, ei, ej, w, m, kind);
+  return cudaGetLastError();
+}
+
 // ---- whole circuit for small states (n <= 11) in ONE CTA -------------------
 // The state (<= 2048 amplitudes, 32 KB) lives in shared memory for all p
 // levels: launch control, per level the cost (cost.py:162-176, FMA-form

@@ -480,6 +480,9 @@ class IpcExchanger:
         from . import _lib
 
         self.shard, self.rank, self.world, self.group = shard, rank, world, group
+        self.timing = False  # set True to time every exchange kernel (CUDA events)
+        self._pending: list = []  # per exchange: its (start, stop) event pairs
+        self.exchange_ms: list[float] = []  # kernel time per exchange, this rank's slice
         handles = [None] * world
         dist.all_gather_object(handles, shard.ipc_handle(), group=group)
         self.ptrs, self.opened = [], []
@@ -507,9 +510,43 @@ class IpcExchanger:
         self._barrier()  # every shard finished the segment before anyone reads it
         import torch
 
+        self._begin_exchange()
+        ev = self._mark(sh.stream)
         _exchange_call(sh.device, sh.stream_ptr, g_bits, self.ptrs, sh.n, p0, lo, hi, rx, factor)
+        self._mark_end(ev, sh.stream)
         torch.cuda.synchronize(sh.device)
+        self.collect()
         self._barrier()  # every write into my shard landed before my next sweep
+
+    # ---- per-exchange kernel timing (CUDA events on the launching stream) -----
+    def _begin_exchange(self):
+        if self.timing:
+            self._pending.append([])
+
+    def _mark(self, stream):
+        if not self.timing:
+            return None
+        import torch
+
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    def _mark_end(self, start, stream):
+        if start is None:
+            return
+        import torch
+
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        self._pending[-1].append((start, e))
+
+    def collect(self) -> None:
+        """Resolve the timed exchanges (call once their streams have synchronised):
+        one entry per exchange = the sum of its kernel launches' durations."""
+        for pairs in self._pending:
+            self.exchange_ms.append(sum(a.elapsed_time(b) for a, b in pairs))
+        self._pending = []
 
     def close(self) -> None:
         from . import _lib
@@ -576,6 +613,7 @@ class IpcChunkExchanger(IpcExchanger):
         sh = self.shard
         cols = 1 << (sh.n - g_bits)
         c, G, r = self.n_chunks, self.world, self.rank
+        self._begin_exchange()
         for t in range(c):
             if self.ipc_events:
                 for rr in range(G):
@@ -584,8 +622,10 @@ class IpcChunkExchanger(IpcExchanger):
                 self.my_pre[t].synchronize()
                 self._host_barrier()
             lo, hi = cols * t // c, cols * (t + 1) // c
+            ev = self._mark(self.xstream)  # after the waits: the chunk's kernel time only
             _exchange_call(sh.device, self.xstream.cuda_stream, g_bits, self.ptrs, sh.n, p0,
                            lo + (hi - lo) * r // G, lo + (hi - lo) * (r + 1) // G, rx, factor)
+            self._mark_end(ev, self.xstream)
             self.my_x[t].record(self.xstream)
 
     def wait_chunk(self, shard_index: int, t: int) -> None:

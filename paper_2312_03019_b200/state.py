@@ -230,20 +230,42 @@ def as_tensor(s: StateVector):
 
 
 def init_zero_state(n: int, max_qubits: int = DEFAULT_MAX_QUBITS) -> StateVector:
-    """|0...0> (state.py:66-72)."""
+    """|0...0>: amplitude 1 at index 0 (state.py:66-72), written on the device."""
     check_qubit_budget(n, max_qubits)
     eng = Engine(n)
-    amps = np.zeros(1 << n, dtype=np.complex128) if n <= 20 else None
-    if amps is not None:
-        amps[0] = 1.0
-        eng.write(amps)
-    else:
-        zero = np.zeros(1 << 20, dtype=np.complex128)
-        for off in range(0, 1 << n, 1 << 20):
-            eng.write(zero, off)
-        eng.write(np.ones(1, dtype=np.complex128), 0)
+    eng.call("qaoa_init_basis", 0)
     write_counter.add(1 << n)
     return StateVector(n, engine=eng)
+
+
+def apply_h(s: StateVector, q: int, threads: int = 1) -> StateVector:
+    """Hadamard on qubit q (state.py:91-107): (a +- b) * (1/sqrt 2) with the
+    reference's rounding, one device pass."""
+    if not 0 <= q < s.n:
+        raise IndexError(f"qubit {q} out of range for n={s.n}")
+    s.engine().call("qaoa_apply_h", int(q))
+    write_counter.add(1 << s.n)
+    return s
+
+
+def rzz_phases(theta: float) -> np.ndarray:
+    """(e_same, e_diff) formed exactly as state.py:138-139 forms them."""
+    return np.array([complex(np.exp(-0.5j * theta)), complex(np.exp(0.5j * theta))],
+                    dtype=np.complex128)
+
+
+def apply_rzz(s: StateVector, q1: int, q2: int, theta: float, threads: int = 1) -> StateVector:
+    """exp(-i theta Z Z / 2) on qubits q1, q2 (state.py:131-149), one device pass,
+    bit-exact (numpy's FMA-form complex multiply)."""
+    if q1 == q2:
+        raise ValueError("RZZ needs two distinct qubits")
+    for q in (q1, q2):
+        if not 0 <= q < s.n:
+            raise IndexError(f"qubit {q} out of range for n={s.n}")
+    ph = rzz_phases(theta)
+    s.engine().call("qaoa_apply_rzz", int(q1), int(q2), _lib.dptr(ph.view(np.float64)))
+    write_counter.add(1 << s.n)
+    return s
 
 
 def apply_rx(s: StateVector, q: int, theta: float, threads: int = 1) -> StateVector:

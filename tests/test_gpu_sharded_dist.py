@@ -37,3 +37,37 @@ def test_torchrun_sharded_bench(world, exchange, chunks, events):
     assert line["expectation"] == pytest.approx(e, rel=1e-10)
     assert line["n_gpus"] == world and line["scaling"] == "strong" and line["test_mode"]
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+
+
+@pytest.mark.parametrize("world,chunks,levels", [(2, 4, 1), (4, 1, 2)])
+def test_torchrun_weak_scaling_modes(world, chunks, levels):
+    """--scaling weak: 2^qubits amplitudes per rank (N = qubits + log2 G, odd N =
+    u3r(N-1) + an isolated node), p=1 checked against the closed form inside the
+    bench, per-exchange kernel times (CUDA events) reported for the NVLink
+    figure; <C> equals the unsharded engine's."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    base = 20
+    n = base + world.bit_length() - 1
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29700 + world + chunks),
+           os.path.join(ROOT, "bench.py"), "--gpus", str(world), "--steps", "2", "--warmup", "3",
+           "--qubits", str(base), "--levels", str(levels), "--dist-backend", "gloo",
+           "--share-device", "--scaling", "weak", "--chunks", str(chunks)]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["scaling"] == "weak" and line["config"]["n_qubits"] == n
+
+    class A:
+        graph = "u3r"
+
+    A.n = n
+    g = bench.make_graph(Q, A)
+    e = Q.expectation(g, Q.simulate(g, Q.params_from_seed(levels, 0), "bitwise", max_qubits=n))
+    assert line["expectation"] == pytest.approx(e, rel=1e-10)
+    if levels == 1:
+        assert line["closed_form_p1"]["rel_err"] <= 1e-10
+    nv = line["nvlink"]
+    assert nv["exchange_ms"] > 0 and nv["achieved_GBps_per_direction"] > 0
