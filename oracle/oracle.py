@@ -53,6 +53,9 @@ def lib():
         L.orc_norm.argtypes = [ctypes.c_int, _f64p, ctypes.c_int]
         L.orc_norm.restype = ctypes.c_double
         L.orc_max_threads.restype = ctypes.c_int
+        L.orc_apply_h.argtypes = [ctypes.c_int, ctypes.c_int, _f64p, ctypes.c_int]
+        L.orc_apply_rzz.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _f64p, _f64p,
+                                    ctypes.c_int]
         L.orc_apply_cost_x.argtypes = [ctypes.c_int, ctypes.c_int, _u64p, ctypes.c_uint64,
                                        ctypes.c_int, _f64p, _f64p, ctypes.c_int]
         L.orc_expectation_x.argtypes = [ctypes.c_int, ctypes.c_int, _u64p, ctypes.c_uint64, _f64p,
@@ -116,6 +119,43 @@ def apply_rx(amps: np.ndarray, n: int, q: int, theta: float, threads: int = 0) -
     """state.py:110-128, in place."""
     lib().orc_apply_rx(n, q, math.cos(theta / 2.0), math.sin(theta / 2.0), _ptr(amps, _f64p),
                        threads)
+    return amps
+
+
+def apply_h(amps: np.ndarray, n: int, q: int, threads: int = 0) -> np.ndarray:
+    """state.py:91-107, in place."""
+    lib().orc_apply_h(n, q, _ptr(amps, _f64p), threads)
+    return amps
+
+
+def apply_rzz(amps: np.ndarray, n: int, q1: int, q2: int, theta: float,
+              threads: int = 0) -> np.ndarray:
+    """state.py:131-149, in place; the two phases formed as the reference forms them."""
+    ph = np.array([complex(np.exp(-0.5j * theta)), complex(np.exp(0.5j * theta))],
+                  dtype=np.complex128)
+    lib().orc_apply_rzz(n, q1, q2, _ptr(ph, _f64p), _ptr(amps, _f64p), threads)
+    return amps
+
+
+def simulate_gates(n: int, edges, gammas, betas, launch_control: bool = True,
+                   threads: int = 0) -> np.ndarray:
+    """simulate(..., backend="baseline"), circuit.py:97-113: init_state
+    (circuit.py:51-62: uniform, or |0..0> plus n Hadamards), then per level one
+    RZZ(w gamma) per edge in edge order (circuit.py:76-80) and RX(-beta) per qubit."""
+    if launch_control:
+        amps = init_uniform(n, threads)
+    else:
+        amps = np.zeros(1 << n, dtype=np.complex128)
+        amps[0] = 1.0
+        for q in range(n):
+            apply_h(amps, n, q, threads)
+    for gm, bt in zip(gammas, betas):
+        for e in edges:
+            i, j = int(e[0]), int(e[1])
+            w = float(e[2]) if len(e) > 2 else 1.0
+            apply_rzz(amps, n, i, j, w * gm, threads)
+        for q in range(n):
+            apply_rx(amps, n, q, -bt, threads)
     return amps
 
 

@@ -113,6 +113,42 @@ ORC_EXPORT void orc_apply_rx(int n, int q, double c, double s, double* amps, int
     }
 }
 
+/* apply_h, state.py:91-107: top = (a + b) * k, bot = (a - b) * k with
+ * k = 1.0 / sqrt(2.0) (state.py:22); numpy multiplies by the scalar as a
+ * complex (k, 0): re*k - im*0 has the value re*k. */
+ORC_EXPORT void orc_apply_h(int n, int q, double* amps, int threads) {
+    const int64_t half = (int64_t)1 << (n - 1);
+    const int64_t stride = (int64_t)1 << q;
+    const double k = 1.0 / sqrt(2.0);
+    threads = set_threads(threads);
+#pragma omp parallel for schedule(static) num_threads(threads)
+    for (int64_t j = 0; j < half; ++j) {
+        const int64_t i0 = ((j >> q) << (q + 1)) | (j & (stride - 1));
+        const int64_t i1 = i0 | stride;
+        const double ar = amps[2 * i0], ai = amps[2 * i0 + 1];
+        const double br = amps[2 * i1], bi = amps[2 * i1 + 1];
+        amps[2 * i0] = (ar + br) * k; amps[2 * i0 + 1] = (ai + bi) * k;
+        amps[2 * i1] = (ar - br) * k; amps[2 * i1 + 1] = (ai - bi) * k;
+    }
+}
+
+/* apply_rzz, state.py:131-149: amps *= where(bit q1 != bit q2, e_diff, e_same),
+ * phases = {e_same.re, e_same.im, e_diff.re, e_diff.im} as numpy forms them;
+ * numpy's FMA-form complex multiply (as in orc_apply_cost). */
+ORC_EXPORT void orc_apply_rzz(int n, int q1, int q2, const double* phases, double* amps,
+                              int threads) {
+    const int64_t size = (int64_t)1 << n;
+    threads = set_threads(threads);
+#pragma omp parallel for schedule(static) num_threads(threads)
+    for (int64_t x = 0; x < size; ++x) {
+        const int d = (int)(((x >> q1) ^ (x >> q2)) & 1);
+        const double pr = phases[2 * d], pi = phases[2 * d + 1];
+        const double ar = amps[2 * x], ai = amps[2 * x + 1];
+        amps[2 * x] = fma(ar, pr, -(ai * pi));
+        amps[2 * x + 1] = fma(ar, pi, ai * pr);
+    }
+}
+
 /* apply_mixer_layer, circuit.py:89-94: RX on every qubit, q = 0..n-1 in order. */
 ORC_EXPORT void orc_apply_mixer(int n, double c, double s, double* amps, int threads) {
     for (int q = 0; q < n; ++q) orc_apply_rx(n, q, c, s, amps, threads);

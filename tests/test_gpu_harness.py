@@ -24,3 +24,17 @@ def test_records_and_compare():
     assert H.parse_generator_spec("er:n=33").tot_edge == 236
     with pytest.raises(ValueError):
         H.parse_generator_spec("u3r:seed=1")
+
+
+def test_compare_gate_level_baseline_vs_fused():
+    """The reference's speedup table (bench.py:184-243): gate-level "baseline"
+    (one device pass per gate) against the fused "bitwise" engine, behind the
+    1e-10 equivalence gate; the baseline's cost and mixer times are split."""
+    rows = H.run_compare([16, 18], ["baseline", "bitwise"],
+                         lambda n: Q.random_regular_graph(n, 3, seed=0), p=2, reps=1)
+    assert len(rows) == 4
+    base = [r for r in rows if r["backend"] == "baseline"]
+    fused = [r for r in rows if r["backend"] == "bitwise"]
+    assert all(r["cost_time_ns"] > 0 and r["mixer_time_ns"] > 0 for r in base)
+    assert all(r["max_abs_diff"] <= 1e-12 for r in fused)
+    assert all(r["total_speedup"] > 1.0 for r in fused)

@@ -104,3 +104,37 @@ def test_oracle_invariants(oracle):
     gm, bt = oracle.params_from_seed(3, 1)
     amps = oracle.simulate(n, rm, len(edges), gm, bt)
     assert oracle.norm(n, amps) == pytest.approx(1.0, abs=1e-13)
+
+
+# ---- gate-level path (backend "baseline", launch_control=False) -------------
+def _gates_golden():
+    import json
+    import os
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    with open(os.path.join(here, "golden_gates.json")) as f:
+        meta = json.load(f)
+    return meta, dict(np.load(os.path.join(here, "golden_gates.npz")))
+
+
+def test_oracle_gate_level_circuits_bit_exact(oracle):
+    """oracle.simulate_gates == the reference's simulate(backend="baseline"),
+    with and without launch control, unweighted and weighted (fixtures made by
+    running the reference, tests/golden/make_golden_gates.py)."""
+    meta, arrays = _gates_golden()
+    for case in meta["cases"]:
+        got = oracle.simulate_gates(case["n"], case["edges"], case["gamma"], case["beta"],
+                                    launch_control=case["launch_control"])
+        assert np.array_equal(got, arrays["amps_" + case["name"]]), case["name"]
+
+
+def test_oracle_single_gates_bit_exact(oracle):
+    meta, arrays = _gates_golden()
+    n = meta["gate_n"]
+    a = arrays["gate_in"].copy()
+    for k, op in enumerate(meta["gates"]):
+        if op[0] == "h":
+            oracle.apply_h(a, n, op[1])
+        else:
+            oracle.apply_rzz(a, n, op[1], op[2], op[3])
+        assert np.array_equal(a, arrays[f"gate_out_{k}"]), op
