@@ -145,6 +145,10 @@ QAOA_API int qaoa_apply_rx_range(qaoa_ctx* ctx, int q0, int count, double c, dou
  * Costs a second 16 B x 2^n device buffer, kept until qaoa_destroy. */
 QAOA_API int qaoa_set_layout_swap(qaoa_ctx* ctx, int mode);
 
+/* Release the context's optional device buffers: the second state buffer of
+ * the swapped layout and the cut table (both are re-allocated on demand). */
+QAOA_API int qaoa_trim(qaoa_ctx* ctx);
+
 /* Complement mask of the stored state: the amplitude of true basis index x is
  * stored at physical index x ^ cmask (fast-mode bookkeeping; bits >= n_local are
  * shard bits maintained by a sharded host).  read/write_amplitudes map the local

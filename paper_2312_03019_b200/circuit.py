@@ -166,6 +166,7 @@ def simulate(
     fuse_expectation: bool = True,
     state: StateVector | None = None,
     store_state: bool = True,
+    layout_swap: int | None = None,
 ) -> StateVector:
     """Run the p-level circuit on the GPU and return the device-resident state
     (circuit.py:97-113).  backend="baseline" (the reference's default) is the
@@ -176,6 +177,9 @@ def simulate(
     Extra keyword-only knobs: ``exact`` (bit-exact reference schedule),
     ``device``, ``fuse_expectation`` (accumulate <C> in the last sweep) and
     ``state`` (reuse a StateVector's device buffer instead of allocating) and
+    ``layout_swap`` (-1 / 0 / 1: the swapped-qubit-layout policy of the
+    state's engine, see ``Engine.set_layout_swap``; the default policy keeps a
+    second 16 B x 2^n device buffer at N=30-type sizes) and
     ``store_state=False`` (only <C> is wanted: the last sweep reads without
     writing back, and the returned state may only be passed to
     ``expectation`` or reused as ``state=``; the optimizer uses it).
@@ -198,6 +202,8 @@ def simulate(
         eng = Engine(g.n, device)
         s = StateVector(g.n, engine=eng)
     eng.ensure_graph(g)
+    if layout_swap is not None:
+        eng.set_layout_swap(layout_swap)
     from_state = 0
     if not launch_control:
         _init_on(eng, g.n)

@@ -467,7 +467,7 @@ int create_common(int n, int device, void* stream, void* ext, qaoa_ctx** out) {
 // cmask covers the shard bits too), <C> is fused only when the run does not end
 // on an exchange.
 int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, const double* sn,
-              int flags, bool sharded, const double* gammas = nullptr) {
+              int flags, bool sharded, const double* gammas = nullptr, bool internal = false) {
   RunState& R = c->run;
   R = RunState();
   R.weighted = gammas != nullptr;
@@ -604,7 +604,12 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
     CUDA_TRY(launch_wc_table(c->d_wc, c->d_wedge, c->d_w, c->n_wedges, sd.carry, sd.q, c->stream));
   }
   R.no_store_last = (flags & QAOA_RUN_EXPECT_ONLY) && R.expect_fused;
-  plan_swaps(c, R);
+  // the swapped layout only for runs the library drives end to end
+  // (qaoa_run_layers*): hosts of qaoa_run_begin see every sweep in place, so
+  // qaoa_run_sweep_info geometry, partial ranges and graph / mask changes
+  // between segments stay valid
+  if (internal) plan_swaps(c, R);
+  else R.swap = false;
   R.active = true;
   if ((rc = record_event(c, R.timing, R.ev++))) return rc;
   return QAOA_OK;
@@ -913,6 +918,22 @@ int qaoa_read_amplitudes(qaoa_ctx* c, uint64_t offset, uint64_t count, double* d
   return QAOA_OK;
 }
 
+int qaoa_trim(qaoa_ctx* c) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (c->run.active) return fail(QAOA_E_STATE, "a planned run is active");
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (c->amps2) {
+    cudaFree(c->amps2);
+    c->amps2 = nullptr;
+  }
+  if (c->cut_table) {
+    cudaFree(c->cut_table);
+    c->cut_table = nullptr;
+  }
+  return QAOA_OK;
+}
+
 int qaoa_set_layout_swap(qaoa_ctx* c, int mode) {
   int rc = check_ctx(c);
   if (rc) return rc;
@@ -1174,7 +1195,7 @@ int qaoa_run_layers(qaoa_ctx* c, int p, const double* phase_tables, const double
   }
 
   // ---- tiled path --------------------------------------------------------
-  if ((rc = run_begin(c, p, phase_tables, cs, sn, flags, false))) return rc;
+  if ((rc = run_begin(c, p, phase_tables, cs, sn, flags, false, nullptr, true))) return rc;
   if (p == 0) return QAOA_OK;  // handled (fill / expectation) inside run_begin
   for (size_t k = 0; k + 1 < c->run.seg_start.size(); ++k)
     if ((rc = run_segment(c, (int)k))) return rc;
@@ -1214,7 +1235,7 @@ int qaoa_run_layers_weighted(qaoa_ctx* c, int p, const double* gammas, const dou
   if (c->n < 12) return fail(QAOA_E_INVALID, "the factored weighted schedule needs at least 12 qubits");
   if (flags & (QAOA_RUN_EXACT | QAOA_RUN_SHARDED))
     return fail(QAOA_E_INVALID, "the factored weighted schedule is fast-mode and unsharded only");
-  if ((rc = run_begin(c, p, nullptr, cs, sn, flags, false, gammas))) return rc;
+  if ((rc = run_begin(c, p, nullptr, cs, sn, flags, false, gammas, true))) return rc;
   for (size_t k = 0; k + 1 < c->run.seg_start.size(); ++k)
     if ((rc = run_segment(c, (int)k))) return rc;
   return run_end(c);

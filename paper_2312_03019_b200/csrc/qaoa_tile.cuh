@@ -210,13 +210,17 @@ struct TileCtx {
 // (x_hi ^ cmask ^ base, see GraphDev::cmask); K = C(h); per tile node k,
 // d[k] = deg(k) - 2 popc(adj[k] & h) (change of C when node k alone is set);
 // adjl[k] = tile-local neighbour mask (12 bits); tmask = cmask's tile bits (the
-// true tile bits of tile index t are t ^ tmask).
-struct CutBasis {
+// true tile bits of tile index t are t ^ tmask).  Packed so a thread reads the
+// whole basis with four broadcast loads: pk[k] = d[k] << 16 | adjl[k].
+struct __align__(16) CutBasis {
+  int pk[12];
   int K;
   int tmask;
-  int d[12];
-  int adjl[12];
 };
+
+__device__ __forceinline__ int pack_basis(int d, int adjl) {
+  return (int)(((unsigned)d << 16) | (unsigned)adjl);
+}
 
 template <bool WIDE, int C>
 __device__ __forceinline__ void cut_basis(const SweepArgs& a, uint64_t base, int q, CutBasis* cb) {
@@ -238,10 +242,9 @@ __device__ __forceinline__ void cut_basis(const SweepArgs& a, uint64_t base, int
   if (lane < 12) {
     const int p = tile_pos<C>(lane, q);
     const uint64_t m = a.g.adj[p];
-    cb->d[lane] = __popcll(m) - 2 * __popcll(m & h);
     const uint32_t lo = (uint32_t)(m & ((C >= 12) ? 0xFFFull : ((1ull << C) - 1ull)));
     const uint32_t hi = (C >= 12) ? 0u : (uint32_t)((m >> q) & ((1ull << (12 - C)) - 1ull)) << C;
-    cb->adjl[lane] = (int)(lo | hi);
+    cb->pk[lane] = pack_basis(__popcll(m) - 2 * __popcll(m & h), (int)(lo | hi));
   }
   if (lane == 0) {
     cb->K = part;
@@ -254,28 +257,52 @@ __device__ __forceinline__ void cut_basis(const SweepArgs& a, uint64_t base, int
 // flipping register node j changes C by s_j (d[j] - 2 popc(adjl[j] & T)) with
 // s_j = -1 if bit j of T is set, and each edge between two flipped nodes j, k
 // adds -2 s_j s_k.  Exact integer arithmetic.
+struct CutParts {
+  int c0;       // C of the thread's register-0 element
+  int d[4];     // change of C when register bit j alone flips
+  int a[4][4];  // a[j][k] (j < k): -a is the extra change when both flip (0 or +-2)
+};
+
 template <int M>
-__device__ __forceinline__ void cut16(const CutBasis* cb, int (&c)[16], int tid, int sk = 0) {
+__device__ __forceinline__ void cut_parts(const CutBasis* cb, CutParts& cp, int tid, int sk) {
+  // four broadcast loads of the packed basis
+  int pk[12];
+  const int4* p4 = reinterpret_cast<const int4*>(cb->pk);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int4 w = p4[i];
+    pk[4 * i] = w.x; pk[4 * i + 1] = w.y; pk[4 * i + 2] = w.z; pk[4 * i + 3] = w.w;
+  }
+  const int2 kt = *reinterpret_cast<const int2*>(&cb->K);
   // skewed layout: physical register 0 holds logical register sk
-  const int T = tile_index<M>(tid, 0) ^ cb->tmask ^ (sk ? tile_index<M>(0, 1) : 0);
+  const int T = tile_index<M>(tid, 0) ^ kt.y ^ (sk ? tile_index<M>(0, 1) : 0);
   constexpr int g = group_of<M>();
-  int c0 = cb->K;
+  int c0 = kt.x;
 #pragma unroll
   for (int k = 0; k < 12; ++k)
-    if ((T >> k) & 1) c0 += cb->d[k] - __popc(cb->adjl[k] & T);
-  int d[4], al[4], sg[4];
+    if ((T >> k) & 1) c0 += (pk[k] >> 16) - __popc(pk[k] & T);
+  cp.c0 = c0;
+  int al[4], sg[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    al[j] = cb->adjl[4 * g + j];
+    al[j] = pk[4 * g + j] & 0xFFF;
     sg[j] = ((T >> (4 * g + j)) & 1) ? -1 : 1;
-    d[j] = sg[j] * (cb->d[4 * g + j] - 2 * __popc(al[j] & T));
+    cp.d[j] = sg[j] * ((pk[4 * g + j] >> 16) - 2 * __popc(al[j] & T));
   }
-  const int a01 = 2 * sg[0] * sg[1] * ((al[0] >> (4 * g + 1)) & 1);
-  const int a02 = 2 * sg[0] * sg[2] * ((al[0] >> (4 * g + 2)) & 1);
-  const int a03 = 2 * sg[0] * sg[3] * ((al[0] >> (4 * g + 3)) & 1);
-  const int a12 = 2 * sg[1] * sg[2] * ((al[1] >> (4 * g + 2)) & 1);
-  const int a13 = 2 * sg[1] * sg[3] * ((al[1] >> (4 * g + 3)) & 1);
-  const int a23 = 2 * sg[2] * sg[3] * ((al[2] >> (4 * g + 3)) & 1);
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int k = j + 1; k < 4; ++k) cp.a[j][k] = 2 * sg[j] * sg[k] * ((al[j] >> (4 * g + k)) & 1);
+}
+
+template <int M>
+__device__ __forceinline__ void cut16(const CutBasis* cb, int (&c)[16], int tid, int sk = 0) {
+  CutParts cp;
+  cut_parts<M>(cb, cp, tid, sk);
+  const int c0 = cp.c0;
+  const int(&d)[4] = cp.d;
+  const int a01 = cp.a[0][1], a02 = cp.a[0][2], a03 = cp.a[0][3];
+  const int a12 = cp.a[1][2], a13 = cp.a[1][3], a23 = cp.a[2][3];
   c[0] = c0;
   c[1] = c0 + d[0];
   c[2] = c0 + d[1];
@@ -472,14 +499,28 @@ __device__ __forceinline__ void apply_wcost(double2 (&v)[kRegs], const WBasis* w
 
 // amp *= table_even[E - C(x)] (table_even[k] = phase_table[2k]; reference
 // cost.py:168-172 indexes table[(E - 2C) + E]).
+#ifndef QB_SKIP
+#define QB_SKIP 0
+#endif
 template <int M>
 __device__ __forceinline__ void apply_cost(double2 (&v)[kRegs], const CutBasis* cb,
                                            const double2* __restrict__ tab, int e,
                                            int tid = threadIdx.x, int sk = 0) {
   int c[16];
-  cut16<M>(cb, c, tid, sk);
+  if (QB_SKIP & 32) {  // probe builds only: no cut counts
 #pragma unroll
-  for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], __ldg(tab + (e - c[r])));
+    for (int r = 0; r < kRegs; ++r) c[r] = (tid + r) & 15;
+  } else {
+    cut16<M>(cb, c, tid, sk);
+  }
+  if (QB_SKIP & 16) {  // probe builds only: no table gather
+    const double2 p0 = __ldg(tab + e);
+#pragma unroll
+    for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], make_double2(p0.x + c[r], p0.y));
+  } else {
+#pragma unroll
+    for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], __ldg(tab + (e - c[r])));
+  }
 }
 
 template <int M>
@@ -560,6 +601,13 @@ __device__ __forceinline__ void store_tile(double2* __restrict__ amps, const Til
 template <int V>
 using ic = std::integral_constant<int, V>;
 
+// Timing-decomposition switches for tools/sweep_probe builds only (the library
+// is built with QB_SKIP = 0): bit 0 skips the shared-memory exchanges, bit 1
+// the lane transposes, bit 2 the cost phase, bit 3 the RX butterflies; inside
+// the cost (apply_cost) bit 4 the table gather, bit 5 the cut counts.
+constexpr bool kDoX = !(QB_SKIP & 1), kDoT = !(QB_SKIP & 2), kDoC = !(QB_SKIP & 4),
+               kDoR = !(QB_SKIP & 8);
+
 template <int C, int FLOW>
 __host__ __device__ constexpr int fast_last() {
   return C >= 12 ? (FLOW == 2 ? 2 : 1) : ((Act<C>::g1 && FLOW == 1) ? 1 : 2);
@@ -574,55 +622,55 @@ __device__ __forceinline__ void fast_tile(double2 (&v)[kRegs], const SweepArgs& 
   const double r1a = a.rx1.a, r2a = a.rx2.a;
   if (a.flags & kPreCost) {
     if (WGT) apply_wcost<2>(v, &wb[0], a.wq1, tid, sk);
-    else apply_cost<2>(v, cb, a.table, e, tid, sk);
+    else if (kDoC) apply_cost<2>(v, cb, a.table, e, tid, sk);
   }
   if (C >= 12) {
     // low set: G2 (loaded), G0, G1 [, cost, G1, G0, G2]
-    rx_regs2<A::g2, false>(v, r1a, 0.0);
-    xchg(ic<2>(), ic<0>());
-    rx_regs2<A::g0, false>(v, r1a, 0.0);
-    xchg(ic<0>(), ic<1>());
-    rx_regs2<A::g1, false>(v, r1a, 0.0);
+    if (kDoR) rx_regs2<A::g2, false>(v, r1a, 0.0);
+    if (kDoX) xchg(ic<2>(), ic<0>());
+    if (kDoR) rx_regs2<A::g0, false>(v, r1a, 0.0);
+    if (kDoX) xchg(ic<0>(), ic<1>());
+    if (kDoR) rx_regs2<A::g1, false>(v, r1a, 0.0);
     if (FLOW == 2) {
       if (WGT) apply_wcost<1>(v, &wb[1], a.wq2, tid, sk);
-      else apply_cost<1>(v, cb, a.table2, e, tid, sk);
-      rx_regs2<A::g1, false>(v, r2a, 0.0);
-      xchg(ic<1>(), ic<0>());
-      rx_regs2<A::g0, false>(v, r2a, 0.0);
-      xchg(ic<0>(), ic<2>());
-      rx_regs2<A::g2, false>(v, r2a, 0.0);
+      else if (kDoC) apply_cost<1>(v, cb, a.table2, e, tid, sk);
+      if (kDoR) rx_regs2<A::g1, false>(v, r2a, 0.0);
+      if (kDoX) xchg(ic<1>(), ic<0>());
+      if (kDoR) rx_regs2<A::g0, false>(v, r2a, 0.0);
+      if (kDoX) xchg(ic<0>(), ic<2>());
+      if (kDoR) rx_regs2<A::g2, false>(v, r2a, 0.0);
     }
   } else {
     // high set: G2 (+ tile bit 3), G1 [, cost, G1 (+ tile bit 3), G2]
-    rx_regs2<A::g2, false>(v, r1a, 0.0);
+    if (kDoR) rx_regs2<A::g2, false>(v, r1a, 0.0);
     if (A::g0_shfl) {  // C = 3: tile bit 3 traded into register bit 0 (M2 -> M3)
-      transpose_lane3_sk(v);
-      rx_regs2<1u, false>(v, r1a, 0.0);
-      xchg(ic<3>(), ic<1>());
-      rx_regs2<A::g1, false>(v, r1a, 0.0);
+      if (kDoT) transpose_lane3_sk(v);
+      if (kDoR) rx_regs2<1u, false>(v, r1a, 0.0);
+      if (kDoX) xchg(ic<3>(), ic<1>());
+      if (kDoR) rx_regs2<A::g1, false>(v, r1a, 0.0);
       if (FLOW == 2) {
         if (WGT) apply_wcost<1>(v, &wb[1], a.wq2, tid, sk);
-        else apply_cost<1>(v, cb, a.table2, e, tid, sk);
-        rx_regs2<A::g1, false>(v, r2a, 0.0);
-        transpose_lane3_sk(v);  // M1 -> M4
-        rx_regs2<1u, false>(v, r2a, 0.0);
-        xchg(ic<4>(), ic<2>());
-        rx_regs2<A::g2, false>(v, r2a, 0.0);
+        else if (kDoC) apply_cost<1>(v, cb, a.table2, e, tid, sk);
+        if (kDoR) rx_regs2<A::g1, false>(v, r2a, 0.0);
+        if (kDoT) transpose_lane3_sk(v);  // M1 -> M4
+        if (kDoR) rx_regs2<1u, false>(v, r2a, 0.0);
+        if (kDoX) xchg(ic<4>(), ic<2>());
+        if (kDoR) rx_regs2<A::g2, false>(v, r2a, 0.0);
       }
     } else if (A::g1) {
-      xchg(ic<2>(), ic<1>());
-      rx_regs2<A::g1, false>(v, r1a, 0.0);
+      if (kDoX) xchg(ic<2>(), ic<1>());
+      if (kDoR) rx_regs2<A::g1, false>(v, r1a, 0.0);
       if (FLOW == 2) {
         if (WGT) apply_wcost<1>(v, &wb[1], a.wq2, tid, sk);
-        else apply_cost<1>(v, cb, a.table2, e, tid, sk);
-        rx_regs2<A::g1, false>(v, r2a, 0.0);
-        xchg(ic<1>(), ic<2>());
-        rx_regs2<A::g2, false>(v, r2a, 0.0);
+        else if (kDoC) apply_cost<1>(v, cb, a.table2, e, tid, sk);
+        if (kDoR) rx_regs2<A::g1, false>(v, r2a, 0.0);
+        if (kDoX) xchg(ic<1>(), ic<2>());
+        if (kDoR) rx_regs2<A::g2, false>(v, r2a, 0.0);
       }
     } else if (FLOW == 2) {
       if (WGT) apply_wcost<2>(v, &wb[1], a.wq2, tid, sk);
-      else apply_cost<2>(v, cb, a.table2, e, tid, sk);
-      rx_regs2<A::g2, false>(v, r2a, 0.0);
+      else if (kDoC) apply_cost<2>(v, cb, a.table2, e, tid, sk);
+      if (kDoR) rx_regs2<A::g2, false>(v, r2a, 0.0);
     }
   }
   if (a.flags & kScale) {

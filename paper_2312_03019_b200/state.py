@@ -83,6 +83,16 @@ class Engine:
         except Exception:
             pass
 
+    def set_layout_swap(self, mode: int) -> None:
+        """Swapped qubit layout policy of qaoa_run_layers (qaoa_set_layout_swap):
+        -1 default (on at N=30-type sizes when a second 16 B x 2^n buffer fits),
+        0 never (in place, no second buffer), 1 whenever applicable."""
+        self.call("qaoa_set_layout_swap", int(mode))
+
+    def trim(self) -> None:
+        """Free the second state buffer and the cut table (qaoa_trim)."""
+        self.call("qaoa_trim")
+
     def call(self, name: str, *args) -> None:
         _lib.check(getattr(self._L, name)(self.ptr, *args))
 

@@ -110,7 +110,7 @@ def test_gates_on_complemented_state(oracle):
     (second RX form) act on the true state."""
     n = 14
     g = Q.random_regular_graph(n, 3, seed=3)
-    pr = Q.QaoaParams((0.7, 1.3), (2.9, 3.0))  # |sin| > |cos|: complemented storage
+    pr = Q.QaoaParams((0.7, 1.3), (2.9, 0.4))  # one second-form level: complemented storage
     s = Q.simulate(g, pr, "bitwise", max_qubits=n)
     from paper_2312_03019_b200 import _lib
     import ctypes

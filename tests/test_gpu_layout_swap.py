@@ -147,13 +147,12 @@ def test_layout_swap_rejects_bad_mode():
         eng.close()
 
 
-def test_swapped_layout_refuses_partial_ranges_of_out_of_place_sweeps():
-    """qaoa_run_sweep_range on an unsharded swapped run: whole ranges work (the
-    result equals qaoa_run_layers), a partial range of an out-of-place low-set
-    sweep is refused instead of visiting the wrong tiles."""
+def test_host_driven_runs_stay_in_place():
+    """Runs driven through qaoa_run_begin / qaoa_run_sweep_range never use the
+    swapped layout (only qaoa_run_layers does): every sweep, the low set's
+    included, accepts partial tile ranges, and two halves per sweep give the
+    swapped qaoa_run_layers result bit for bit."""
     import torch
-
-    from paper_2312_03019_b200._lib import EngineError
 
     n, p = 24, 2
     g = Q.random_regular_graph(n, 3, seed=4)
@@ -176,12 +175,14 @@ def test_swapped_layout_refuses_partial_ranges_of_out_of_place_sweeps():
                                        ctypes.byref(q), ctypes.byref(nt))
             if rc == _lib.QAOA_E_RANGE:
                 break
-            if carry.value == 12:  # the out-of-place low-set sweep
-                with pytest.raises(EngineError, match="partial"):
-                    eng.call("qaoa_run_sweep_range", i, 0, nt.value // 2)
-            eng.call("qaoa_run_sweep_range", i, 0, nt.value)
+            half = nt.value // 2
+            eng.call("qaoa_run_sweep_range", i, 0, half)
+            eng.call("qaoa_run_sweep_range", i, half, nt.value - half)
             i += 1
         eng.call("qaoa_run_end")
+        assert torch.equal(_state(eng, n), ref)
+        eng.trim()  # frees the second buffer; the next swapped run re-allocates it
+        _run(eng, g, params, 1)
         assert torch.equal(_state(eng, n), ref)
     finally:
         eng.close()

@@ -5,7 +5,7 @@ N=${3:-30}
 nvidia-smi --query-gpu=clocks.sm,power.draw --format=csv,noheader,nounits -lms 100 > /tmp/pw_$$.log &
 P=$!
 sleep 0.5
-tools/sweep_probe $N 400 $1 $2
+${PROBE:-tools/sweep_probe} $N ${REPS:-400} $1 $2
 kill $P
 python3 - /tmp/pw_$$.log <<'PY'
 import sys, statistics

@@ -16,7 +16,7 @@ for n, p in [(int(a.split(':')[0]), int(a.split(':')[1])) for a in (sys.argv[1:]
     eng.ensure_graph(g)
     for exact in (False, True):
         flags = _lib.RUN_EXPECTATION | _lib.RUN_TIMING | (_lib.RUN_EXACT if exact else 0)
-        for it in range(3):
+        for it in range(int(os.environ.get("QB_ITERS", "3"))):
             t0 = time.perf_counter()
             eng.call("qaoa_run_layers", p, _lib.dptr(tables.view(np.float64)), _lib.dptr(cs), _lib.dptr(ss), flags)
             wall = time.perf_counter() - t0
