@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         }
       }
     }
-    walk_tile<C, 2>(amps + tc.base + tc.tb2, Q, sk, [&](int r, double2* ptr) { v[r] = __ldcs(ptr); });
+    walk_tile<C, 2>(amps + tc.base + tc.tb2, Q, sk, [&](int r, double2* ptr) { v[r] = ld_tile(ptr); });
   }
   const bool need_cut = flags & (kPreCost | kMidCost | kExpect);
   if (need_cut) {

@@ -497,6 +497,32 @@ __device__ __forceinline__ void apply_wcost(double2 (&v)[kRegs], const WBasis* w
   }
 }
 
+// Cache policy of the tile stream and the phase-table gathers (QB_LDMODE, A/B
+// builds): 0 = ld.global.cs / ld.global.nc; 1 (default) = tile loads
+// L1::no_allocate: the streaming tile never displaces the phase table from L1
+// (merged sweep 7.23 -> 7.12 ms, tools/decomp_ld.sh); 2 = 1 + table gathers
+// L1::evict_last (no further change).
+#ifndef QB_LDMODE
+#define QB_LDMODE 1
+#endif
+__device__ __forceinline__ double2 ld_tile(const double2* p) {
+  if (QB_LDMODE >= 1) {
+    double2 v;
+    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+  }
+  return __ldcs(p);
+}
+__device__ __forceinline__ double2 ld_phase(const double2* p) {
+  if (QB_LDMODE >= 2) {
+    double2 v;
+    asm("ld.global.nc.L1::evict_last.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+  }
+  return __ldg(p);
+}
+
 // amp *= table_even[E - C(x)] (table_even[k] = phase_table[2k]; reference
 // cost.py:168-172 indexes table[(E - 2C) + E]).
 #ifndef QB_SKIP
@@ -519,7 +545,7 @@ __device__ __forceinline__ void apply_cost(double2 (&v)[kRegs], const CutBasis* 
     for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], make_double2(p0.x + c[r], p0.y));
   } else {
 #pragma unroll
-    for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], __ldg(tab + (e - c[r])));
+    for (int r = 0; r < kRegs; ++r) v[r] = cmul_np(v[r], ld_phase(tab + (e - c[r])));
   }
 }
 

@@ -1,0 +1,10 @@
+#!/bin/bash
+# sweep_probe builds with the cache-policy variants QB_LDMODE (qaoa_tile.cuh).
+cd "$(dirname "$0")/.."
+F="-O3 -gencode arch=compute_100a,code=sm_100a -std=c++17 --expt-relaxed-constexpr -lcuda"
+for k in "$@"; do
+  nvcc $F -DQB_LDMODE=$k -I paper_2312_03019_b200/csrc tools/sweep_probe.cu paper_2312_03019_b200/csrc/qaoa_sweep.cu \
+    paper_2312_03019_b200/csrc/qaoa_sweep_tma.cu paper_2312_03019_b200/csrc/qaoa_cut_table.cu \
+    -o tools/ablib/sweep_probe_ld$k &
+done
+wait
