@@ -25,13 +25,26 @@
 // apply_rx (state.py:110-128) on the arriving qubits, mixer circuit.py:89-94.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "qaoa_common.cuh"
 #include "qaoa_sweep.h"
 
 namespace qb {
 
-template <int G>
+// Peer-load flavour (QAOA_XCHG_LD, A/B): 0 = ld.global.cv (volatile, system
+// scope: never served from a cache), 1 = ld.global.cg (L2 only), 2 = ld.global.nc.
+// All three are correct: the peers' writes completed before the host barrier
+// that precedes this launch, L1 starts every kernel empty, and no element is
+// read after another CTA wrote it inside one launch (see above).
+template <int LD>
+__device__ __forceinline__ double2 ld_peer(const double2* p) {
+  if (LD == 0) return __ldcv(p);
+  if (LD == 1) return __ldcg(p);
+  return __ldg(p);
+}
+
+template <int G, int LD>
 __global__ void __launch_bounds__(256) exchange_kernel(ExchangeArgs a) {
   constexpr int YB = 256 / G;  // y values per CTA (consecutive: coalesced runs)
   const int h = threadIdx.x / YB;
@@ -43,7 +56,7 @@ __global__ void __launch_bounds__(256) exchange_kernel(ExchangeArgs a) {
   double2 v[G];
   if (live) {
 #pragma unroll
-    for (int r = 0; r < G; ++r) v[r] = __ldcv(a.shards[r] + (ybase | ((uint64_t)h << a.p0)));
+    for (int r = 0; r < G; ++r) v[r] = ld_peer<LD>(a.shards[r] + (ybase | ((uint64_t)h << a.p0)));
     // butterflies over the g arriving qubits (bit k of r), increasing k
 #pragma unroll
     for (int k = 0; (1 << k) < G; ++k) {
@@ -66,6 +79,28 @@ __global__ void __launch_bounds__(256) exchange_kernel(ExchangeArgs a) {
   }
 }
 
+template <int LD>
+static cudaError_t launch_ld(const ExchangeArgs& a, unsigned grid, cudaStream_t s) {
+  switch (1 << a.g) {
+    case 2: exchange_kernel<2, LD><<<grid, 256, 0, s>>>(a); break;
+    case 4: exchange_kernel<4, LD><<<grid, 256, 0, s>>>(a); break;
+    case 8: exchange_kernel<8, LD><<<grid, 256, 0, s>>>(a); break;
+    case 16: exchange_kernel<16, LD><<<grid, 256, 0, s>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+static int xchg_ld_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("QAOA_XCHG_LD");
+    v = e ? atoi(e) : 0;
+    if (v < 0 || v > 2) v = 0;
+  }
+  return v;
+}
+
 cudaError_t launch_exchange(const ExchangeArgs& a, cudaStream_t s) {
   if (a.y_hi <= a.y_lo) return cudaSuccess;
   const int G = 1 << a.g;
@@ -73,14 +108,11 @@ cudaError_t launch_exchange(const ExchangeArgs& a, cudaStream_t s) {
   const int yb = 256 / G;
   const uint64_t grid = (count + yb - 1) / yb;
   if (grid > 0x7fffffffull) return cudaErrorInvalidValue;
-  switch (G) {
-    case 2: exchange_kernel<2><<<(unsigned)grid, 256, 0, s>>>(a); break;
-    case 4: exchange_kernel<4><<<(unsigned)grid, 256, 0, s>>>(a); break;
-    case 8: exchange_kernel<8><<<(unsigned)grid, 256, 0, s>>>(a); break;
-    case 16: exchange_kernel<16><<<(unsigned)grid, 256, 0, s>>>(a); break;
-    default: return cudaErrorInvalidValue;
+  switch (xchg_ld_mode()) {
+    case 1: return launch_ld<1>(a, (unsigned)grid, s);
+    case 2: return launch_ld<2>(a, (unsigned)grid, s);
+    default: return launch_ld<0>(a, (unsigned)grid, s);
   }
-  return cudaGetLastError();
 }
 
 }  // namespace qb
