@@ -294,6 +294,30 @@ def run_reference(args, rank: int, world: int):
     return 0
 
 
+def sweep_kinds(L, n: int, p: int, exact: bool, count: int) -> list[str]:
+    """Kind of every sweep of one qaoa_run_layers call, from the engine's own
+    plan export (qaoa_plan: carry, q, pre-cost, stage 1, mid-cost, stage 2,
+    exchange per sweep)."""
+    if n < 12:
+        return ["whole circuit in one CTA"] * count
+    buf = (ctypes.c_int * (7 * 256))()
+    ns = L.qaoa_plan(n, p, 1 if exact else 0, buf, 256)
+    kinds = []
+    for i in range(max(ns, 0)):
+        carry, _q, _pre, _s1, mid = buf[7 * i:7 * i + 5]
+        if i == 0:
+            kinds.append("launch-control sweep (no load)")
+        elif mid >= 0:
+            kinds.append("merged level-boundary sweep")
+        elif i == ns - 1:
+            kinds.append("last sweep (+<C>)")
+        elif carry == 12:
+            kinds.append("low-set sweep S0")
+        else:
+            kinds.append("single high-set sweep")
+    return kinds if len(kinds) == count else ["sweep"] * count
+
+
 def p1_closed_form(n: int, edges, gamma: float, beta: float) -> float:
     """<C> of a p=1 circuit on any unweighted graph, edge by edge (Wang, Hadfield,
     Jiang, Rieffel 2018, mapped to the reference's convention).
@@ -565,24 +589,46 @@ def run_ours(args, rank: int, world: int, local: int):
     sweep_bytes = hb.value  # algorithmic bytes of the last step's sweeps
     sweeps_per_step = len(launch_ms) // max(args.steps, 1)
 
-    # ---- roofline of the sweep kernel (the only kernel on the step's path
-    # apart from one tiny partial-sum reduction) ------------------------------
+    # ---- roofline of the dominant kernel: the sweeps of one step classified by
+    # the engine's own plan (qaoa_plan), the kind with the largest share of the
+    # step is the line's `roofline`; the all-sweeps average is kept beside it ----
     peak, peak_kind = measured_peaks()
     step_sweep_ms = sum(launch_ms) / max(args.steps, 1)
     achieved = sweep_bytes / (step_sweep_ms * 1e-3) / 1e9
     traffic = ncu_traffic(n)
     r_star = 1 + -(-max(0, n - 13) // 10)
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic,
+    last = launch_ms[-sweeps_per_step:]
+    kinds = sweep_kinds(L, n, p, args.exact, len(last))
+    per_kind = {}
+    for kind, ms in zip(kinds, last):
+        d = per_kind.setdefault(kind, {"launches_per_step": 0, "ms": 0.0})
+        d["launches_per_step"] += 1
+        d["ms"] += ms
+    for kind, d in per_kind.items():
+        b = (16 if kind.startswith("launch-control") else 32) * (1 << n)
+        d["avg_ms"] = d["ms"] / d["launches_per_step"]
+        d["share"] = d["ms"] / sum(last)
+        d["GBps"] = b / (d["avg_ms"] * 1e-3) / 1e9
+        d["frac"] = d["GBps"] / peak
+        d["algorithmic_bytes_per_launch"] = b
+    dom = max(per_kind, key=lambda k: per_kind[k]["ms"]) if per_kind else None
+    dk = per_kind.get(dom, {"GBps": achieved, "frac": achieved / peak, "avg_ms": None,
+                            "algorithmic_bytes_per_launch": 32 * (1 << n)})
+    roofline = {"bound": "hbm", "achieved": dk["GBps"], "peak": peak, "unit": "GB/s",
+                "frac": dk["frac"], "traffic": traffic if dom and "merged" in dom else None,
                 "peak_kind": peak_kind,
-                "kernel": "fused cost+RX sweeps (qb::sweep_kernel one tile per CTA + L2 prefetch, "
-                          "low-set sweeps out of place into the swapped qubit layout; "
-                          "qb::sweep_tma_kernel persistent TMA-fed for the launch-control sweep "
-                          "and merges on a top set)",
-                "launch_ms_last_step": [round(x, 3) for x in launch_ms[-sweeps_per_step:]],
-                "algorithmic_bytes_per_launch": 32 * (1 << n),
-                "launches_per_step": sweeps_per_step,
-                "avg_launch_ms": step_sweep_ms / max(sweeps_per_step, 1),
+                "kernel": f"{dom}: qb::sweep_kernel (one 4096-amplitude tile per CTA, two CTAs per "
+                          "SM, L2 tile prefetch; RX on both levels' set, the next level's cost "
+                          "between them)" if dom else "fused sweeps",
+                "algorithmic_bytes_per_launch": dk["algorithmic_bytes_per_launch"],
+                "avg_launch_ms": dk["avg_ms"],
+                "per_kind": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv)
+                                 for kk, vv in d.items()} for k, d in per_kind.items()},
+                # every sweep of the step together (21 at N=30 p=10)
+                "all_sweeps": {"achieved": achieved, "frac": achieved / peak,
+                               "avg_launch_ms": step_sweep_ms / max(sweeps_per_step, 1),
+                               "launches_per_step": sweeps_per_step},
+                "launch_ms_last_step": [round(x, 3) for x in last],
                 # whole-step figures against B_alg = 32 R* 2^N per
                 # level (R* = sweeps of a 2^13 tile) and against the one-pass floor
                 "r_star": r_star,

@@ -34,3 +34,16 @@ def test_r_star_formula():
     # R*(N) = 1 + ceil(max(0, N - 13) / 10)
     r = lambda n: 1 + -(-max(0, n - 13) // 10)  # noqa: E731  (the expression bench.py uses)
     assert [r(n) for n in (12, 13, 20, 23, 24, 26, 30, 33, 34)] == [1, 1, 2, 2, 3, 3, 3, 3, 4]
+
+
+def test_sweep_kinds_from_the_engine_plan():
+    """The bench's roofline picks the dominant sweep kind from qaoa_plan (CPU,
+    no device): N=30 p=10 is 1 launch-control + 10 low-set + 9 merged + 1 last."""
+    import bench
+    from paper_2312_03019_b200 import _lib
+
+    kinds = bench.sweep_kinds(_lib.load(), 30, 10, False, 21)
+    assert kinds[0].startswith("launch-control") and kinds[-1].startswith("last")
+    assert kinds.count("merged level-boundary sweep") == 9
+    assert kinds.count("low-set sweep S0") == 10
+    assert bench.sweep_kinds(_lib.load(), 30, 10, False, 20) == ["sweep"] * 20
