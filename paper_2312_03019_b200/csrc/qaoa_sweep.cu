@@ -117,7 +117,11 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
       if (WGT && (flags & kExpect)) wcut_basis<C>(a, tc.base, q, &wcb[0]);
       if (!WGT) cut_basis<WIDE, C>(a, tc.base, q, &cb);
     }
-    __syncthreads();
+    // The basis is first read after the fast flow's first register exchange
+    // (whose barrier then publishes it) unless a cost step precedes every
+    // exchange: warp 0 builds it while the other warps run the first RX stage.
+    constexpr bool xchg_first = FLOW != 0 && (C >= 12 || Act<C>::g0_shfl || Act<C>::g1 != 0);
+    if (!xchg_first || (flags & kPreCost)) __syncthreads();
   }
   const int e = a.g.tot_edge;
   const double r1a = a.rx1.a, r1b = a.rx1.b;
