@@ -43,6 +43,9 @@ extern "C" {
 #define QAOA_RUN_EXPECTATION 0x4    /* fuse <C> into the last sweep (qaoa_expectation)  */
 #define QAOA_RUN_TIMING 0x8         /* record per-launch CUDA-event times               */
 #define QAOA_RUN_SHARDED 0x10       /* qaoa_run_begin: exchange points after S_0 of every level */
+#define QAOA_RUN_MIRROR 0x40        /* with QAOA_RUN_SHARDED: exact runs put the exchange point
+                                       after the LAST qubit set of each level (the virtual top
+                                       qubit of a symmetric half state, qaoa_mirror_rx) */
 #define QAOA_RUN_EXPECT_ONLY 0x20   /* with QAOA_RUN_EXPECTATION: the last sweep only reads (16 B
                                        instead of 32 B per amplitude); the state is left unusable
                                        (amplitude reads and QAOA_RUN_FROM_STATE then fail) */
@@ -104,6 +107,19 @@ QAOA_API int qaoa_apply_cost(qaoa_ctx* ctx, const double* phase_table);
 /* Single-qubit RX(theta) (apply_rx, state.py:110-128): c = cos(theta/2),
  * s = sin(theta/2).  Bit-exact (products rounded separately). */
 QAOA_API int qaoa_apply_rx(qaoa_ctx* ctx, int qubit, double c, double s);
+
+/* Symmetric half state.  MaxCut QAOA states from launch control (or the
+ * Hadamard chain) keep psi(x) == psi(~x) bit for bit: the uniform start is
+ * symmetric, C(x) == C(~x), and every RX butterfly commutes with the global
+ * flip (its sums are the same products added in the other order).  A context
+ * of n_local qubits with a graph of n_local + 1 nodes then stores the half
+ * x_top = 0 of an (n_local + 1)-qubit state; the top qubit's RX pairs stored
+ * index y with y ^ (2^n_local - 1).  qaoa_mirror_rx applies that RX (rx and
+ * factor as returned by qaoa_run_exchange_info for the level) in one in-place
+ * pass.  Driven by the host at the exchange points of a qaoa_run_begin(...,
+ * QAOA_RUN_SHARDED | QAOA_RUN_MIRROR) run; <C> and the norm of the full state
+ * are twice the half's. */
+QAOA_API int qaoa_mirror_rx(qaoa_ctx* ctx, const double* rx, const double* factor);
 
 /* Gate-level baseline (the reference's default backend "baseline" and
  * init_state(launch_control=False), circuit.py:57-62,76-80).

@@ -32,6 +32,7 @@ RUN_EXPECTATION = 0x4
 RUN_TIMING = 0x8
 RUN_SHARDED = 0x10
 RUN_EXPECT_ONLY = 0x20
+RUN_MIRROR = 0x40
 
 _c_int = ctypes.c_int
 _c_dbl = ctypes.c_double
@@ -64,6 +65,7 @@ SIGNATURES = {
     "qaoa_apply_h": (_c_int, [_vp, _c_int]),
     "qaoa_apply_rzz": (_c_int, [_vp, _c_int, _c_int, _dp]),
     "qaoa_edge_values": (_c_int, [_vp, _c_int, _u64, _u64, _dp]),
+    "qaoa_mirror_rx": (_c_int, [_vp, _dp, _dp]),
     "qaoa_run_layers": (_c_int, [_vp, _c_int, _dp, _dp, _dp, _c_int]),
     "qaoa_apply_rx_range": (_c_int, [_vp, _c_int, _c_int, _c_dbl, _c_dbl, _c_int]),
     "qaoa_set_layout_swap": (_c_int, [_vp, _c_int]),

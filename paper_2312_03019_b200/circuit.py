@@ -167,6 +167,7 @@ def simulate(
     state: StateVector | None = None,
     store_state: bool = True,
     layout_swap: int | None = None,
+    symmetric: bool = False,
 ) -> StateVector:
     """Run the p-level circuit on the GPU and return the device-resident state
     (circuit.py:97-113).  backend="baseline" (the reference's default) is the
@@ -177,7 +178,9 @@ def simulate(
     Extra keyword-only knobs: ``exact`` (bit-exact reference schedule),
     ``device``, ``fuse_expectation`` (accumulate <C> in the last sweep) and
     ``state`` (reuse a StateVector's device buffer instead of allocating) and
-    ``layout_swap`` (-1 / 0 / 1: the swapped-qubit-layout policy of the
+    ``symmetric=True`` (unweighted graphs, launch control, N >= 13: store
+    only the x_{N-1} = 0 half, psi(x) == psi(~x) bit for bit; see
+    ``paper_2312_03019_b200.symmetric``), ``layout_swap`` (-1 / 0 / 1: the swapped-qubit-layout policy of the
     state's engine, see ``Engine.set_layout_swap``; the default policy keeps a
     second 16 B x 2^n device buffer at N=30-type sizes) and
     ``store_state=False`` (only <C> is wanted: the last sweep reads without
@@ -192,6 +195,13 @@ def simulate(
     if batch_width is not None and batch_width not in (1, 2, 4, 8):
         raise ValueError(f"batch width must be 1, 2, 4, or 8, got {batch_width}")
     check_qubit_budget(g.n, max_qubits)
+    if symmetric:
+        if backend == "baseline" or not launch_control or not store_state:
+            raise ValueError("symmetric=True runs the fused engine with launch control")
+        from .symmetric import simulate_symmetric
+
+        return simulate_symmetric(g, params, exact=exact, fuse_expectation=fuse_expectation,
+                                  state=state, device=device)
     if backend == "baseline":
         return _simulate_gates(g, params, launch_control, threads, max_qubits, state)
     if state is not None and state.n == g.n:
@@ -267,6 +277,8 @@ def expectation(g: Graph, s: StateVector) -> float:
     fixed-order reduction; the fused value of the last simulate when valid."""
     if s.n != g.n:
         raise ValueError(f"state has {s.n} qubits but graph has {g.n} nodes")
+    if getattr(s, "half_engine", None) is not None and g.is_unweighted:
+        return s.expectation(g)  # symmetric half state: twice the half's sum
     eng = s.engine()
     eng.ensure_graph(g)
     if not g.is_unweighted:  # float cut values, graph.py:144-151

@@ -227,7 +227,8 @@ std::vector<SetDesc> make_sets(int n) {
   return sets;
 }
 
-std::vector<SweepPlan> make_plan(int n_sets, int p, bool exact, bool sharded = false) {
+std::vector<SweepPlan> make_plan(int n_sets, int p, bool exact, bool sharded = false,
+                                 bool mirror = false) {
   // flat op list: cost l, then mixer l over the sets in this level's order;
   // sharded: an exchange (kind 2) right after the low set S_0 of every level
   // (the swapped local bits sit in S_0, so they have had RX_l when they leave
@@ -255,7 +256,11 @@ std::vector<SweepPlan> make_plan(int n_sets, int p, bool exact, bool sharded = f
     for (int i = 0; i < n_sets; ++i) {
       const int set = fwd ? order[i] : order[n_sets - 1 - i];
       ops.push_back({1, l, set});
-      if (sharded && set == 0) ops.push_back({2, l, -1});
+      // the exchange point: after S_0 (its top bits are the ones a shard
+      // exchange swaps); for the virtual qubit of a symmetric exact run after
+      // the level's last set (the reference applies qubit n last)
+      const int xset = (mirror && exact) ? order[n_sets - 1] : 0;
+      if (sharded && set == xset) ops.push_back({2, l, -1});
     }
   }
   std::vector<SweepPlan> plan;
@@ -491,7 +496,7 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
   if (!R.from_state) c->g.cmask = 0;
 
   R.sets = make_sets(n);
-  R.plan = make_plan((int)R.sets.size(), p, R.exact, sharded);
+  R.plan = make_plan((int)R.sets.size(), p, R.exact, sharded, (flags & QAOA_RUN_MIRROR) != 0);
 
   // phase tables: the sweeps only index even entries (t = E - 2C), so upload
   // table_even[k] = table[2k], k = 0..E.  exact = as given; fast = scaled by
@@ -1030,6 +1035,20 @@ int qaoa_apply_rzz(qaoa_ctx* c, int q1, int q2, const double* phases) {
   const uint64_t xbase = c->g.cmask & ((c->n >= 64) ? ~0ull : ((1ull << c->n) - 1ull));
   CUDA_TRY(launch_rzz_gate(c->amps, 1ull << c->n, xbase, q1, q2, make_double2(phases[0], phases[1]),
                            make_double2(phases[2], phases[3]), c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->expect_valid = false;
+  return QAOA_OK;
+}
+
+int qaoa_mirror_rx(qaoa_ctx* c, const double* rx, const double* factor) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if ((rc = require_stored(c))) return rc;
+  if (!rx || !factor) return fail(QAOA_E_INVALID, "null argument");
+  if (c->n < 2) return fail(QAOA_E_INVALID, "the mirror pass needs at least 2 local qubits");
+  const RxStage st{rx[0], rx[1], (int)rx[2]};
+  const double2 f = make_double2(factor[0], factor[1]);
+  CUDA_TRY(launch_mirror_rx(c->amps, c->n, st, f, !(f.x == 1.0 && f.y == 0.0), c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   c->expect_valid = false;
   return QAOA_OK;

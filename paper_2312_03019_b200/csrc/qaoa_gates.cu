@@ -162,6 +162,38 @@ cudaError_t launch_rzz_gate(double2* amps, uint64_t n, uint64_t xbase, int q1, i
   return cudaGetLastError();
 }
 
+// RX on the virtual top qubit of a symmetric half state: stored index y pairs
+// with y ^ M (M = all local bits), i.e. element y of the first half with the
+// mirrored element of the second half.  mode 0: the reference's butterfly
+// (rx_exact, c / s), mode 1: the factored fast form (t), then `scale` (the
+// level's per-qubit factor) when scale_on.  Thread k handles y = k (bit n-1
+// clear) and its partner; consecutive threads read consecutive y and
+// consecutive (descending) partners, both coalesced.
+__global__ void mirror_rx_kernel(double2* __restrict__ amps, int n_local, RxStage st, double2 scale,
+                                 int scale_on) {
+  const uint64_t half = 1ull << (n_local - 1);
+  const uint64_t M = (1ull << n_local) - 1ull;
+  for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < half;
+       y += (uint64_t)gridDim.x * blockDim.x) {
+    double2 a = amps[y], b = amps[y ^ M];
+    if (st.mode == 0) rx_exact(a, b, st.a, st.b);
+    else rx_form1(a, b, st.a);
+    if (scale_on) {
+      a = cmul_np(a, scale);
+      b = cmul_np(b, scale);
+    }
+    amps[y] = a;
+    amps[y ^ M] = b;
+  }
+}
+
+cudaError_t launch_mirror_rx(double2* amps, int n_local, RxStage st, double2 scale, int scale_on,
+                             cudaStream_t s) {
+  mirror_rx_kernel<<<grid_for(1ull << (n_local - 1), 2), kBlock, 0, s>>>(amps, n_local, st, scale,
+                                                                           scale_on);
+  return cudaGetLastError();
+}
+
 // |index>: zero everywhere, 1 at `index` (init_zero_state, state.py:66-72).
 __global__ void basis_kernel(double2* __restrict__ amps, uint64_t n, uint64_t index) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;

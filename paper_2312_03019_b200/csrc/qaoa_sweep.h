@@ -84,6 +84,8 @@ cudaError_t launch_sweep(const SweepArgs& args, int grid, cudaStream_t stream);
 // simple (per-gate / per-element) kernels, qaoa_gates.cu
 cudaError_t launch_fill(double2* amps, uint64_t n, double2 v, cudaStream_t s);
 cudaError_t launch_basis(double2* amps, uint64_t n, uint64_t index, cudaStream_t s);
+cudaError_t launch_mirror_rx(double2* amps, int n_local, RxStage st, double2 scale, int scale_on,
+                             cudaStream_t s);
 cudaError_t launch_h_gate(double2* amps, int n_local, int q, int flip, cudaStream_t s);
 cudaError_t launch_rzz_gate(double2* amps, uint64_t n, uint64_t xbase, int q1, int q2,
                             double2 e_same, double2 e_diff, cudaStream_t s);

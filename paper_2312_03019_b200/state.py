@@ -291,6 +291,13 @@ def max_abs_diff(a: StateVector, b: StateVector) -> float:
     """max_x |a_x - b_x|, no global-phase quotient (state.py:152-156)."""
     if a.n != b.n:
         raise ValueError(f"qubit counts differ: {a.n} vs {b.n}")
+    ha, hb = getattr(a, "half_engine", None), getattr(b, "half_engine", None)
+    if ha is not None and hb is not None:  # two symmetric halves: their mirrors agree too
+        out = ctypes.c_double()
+        _lib.check(_lib.load().qaoa_max_abs_diff(ha.ptr, hb.ptr, ctypes.byref(out)))
+        return out.value
+    if ha is not None or hb is not None:
+        return float(np.max(np.abs(a.amps - b.amps)))
     if a.on_device and b.on_device:
         out = ctypes.c_double()
         _lib.check(_lib.load().qaoa_max_abs_diff(a._eng.ptr, b._eng.ptr, ctypes.byref(out)))

@@ -1,0 +1,129 @@
+"""Symmetric half-state mode (paper_2312_03019_b200.symmetric): N qubits stored
+as the x_{N-1} = 0 half, the top qubit's RX as one mirror pass per level.
+
+The reference's states are exactly flip-symmetric (psi(x) == psi(~x) bit for
+bit), so the exact schedule on the half must reproduce the reference bit for
+bit once mirrored; the fast schedule stays within the north star's 1e-12."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2312_03019_b200 as Q
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("n,betas", [
+    (13, (0.4, 1.1)),
+    (16, (0.3, 2.9, 1.0)),        # second RX form on one level (fast mode)
+    (21, (2.95, 3.05)),           # odd n: u3r(20) + an isolated node
+    (24, (0.8, 2.2, 3.0, 0.1)),   # three local sets
+])
+def test_symmetric_matches_full_state(oracle, n, betas):
+    g = Q.random_regular_graph(n, 3, seed=n) if n % 2 == 0 else \
+        Q.Graph.from_edges(n, list(Q.random_regular_graph(n - 1, 3, seed=n).edges))
+    gammas = tuple(0.2 + 0.9 * k for k in range(len(betas)))
+    pr = Q.QaoaParams(gammas, betas)
+    ref = oracle.simulate(n, g.row_mask, g.tot_edge, gammas, betas)
+    assert np.array_equal(ref, ref[::-1])  # the reference's state is flip-symmetric bit for bit
+    eref = oracle.expectation(n, g.row_mask, ref)
+    ex = Q.simulate(g, pr, "bitwise", exact=True, symmetric=True, max_qubits=n)
+    assert isinstance(ex, Q.SymmetricState)
+    assert ex.expectation(g) == pytest.approx(eref, rel=1e-10)
+    assert ex.norm() == pytest.approx(1.0, abs=1e-12)
+    assert np.array_equal(ex.amps, ref)
+    fa = Q.simulate(g, pr, "bitwise", symmetric=True, max_qubits=n)
+    assert Q.expectation(g, fa) == pytest.approx(eref, rel=1e-10)
+    assert np.max(np.abs(fa.amps - ref)) <= 1e-12
+
+
+def test_symmetric_golden_n26_sha(golden):
+    """Config C2 (u3r N=26 p=4): the exact schedule on the 2^25 half, mirrored,
+    has the SHA-256 of the reference's own full state."""
+    meta, _ = golden
+    b = next(x for x in meta["big"] if x["key"] == "u3r26_p4")
+    g = Q.random_regular_graph(26, 3, seed=0)
+    pr = Q.params_from_seed(4, 0)
+    s = Q.simulate(g, pr, "bitwise", exact=True, symmetric=True, max_qubits=26)
+    assert Q.expectation(g, s) == pytest.approx(b["expectation"], rel=1e-10)
+    assert sha(s.amps) == b["amps_sha256"]
+
+
+def test_symmetric_state_operations():
+    """copy, max_abs_diff between halves, device materialisation (engine())
+    followed by a single-qubit gate, reuse as state=."""
+    n = 18
+    g = Q.random_regular_graph(n, 3, seed=2)
+    pr = Q.params_from_seed(3, 1)
+    full = Q.simulate(g, pr, "bitwise", max_qubits=n)
+    sym = Q.simulate(g, pr, "bitwise", symmetric=True, max_qubits=n)
+    c = sym.copy()
+    assert Q.max_abs_diff(sym, c) == 0.0
+    assert Q.max_abs_diff(sym, full) <= 1e-12
+    again = Q.simulate(g, pr, "bitwise", symmetric=True, max_qubits=n, state=c)
+    assert again is c and Q.max_abs_diff(again, sym) == 0.0
+    eng = sym.engine()  # full-size device copy
+    assert eng.n == n and not isinstance(sym.half_engine, Q.Engine)
+    Q.apply_rx(sym, 3, 0.7)
+    Q.apply_rx(full, 3, 0.7)
+    assert Q.max_abs_diff(sym, full) <= 1e-12
+    with pytest.raises(ValueError):
+        Q.simulate(g, pr, "bitwise", symmetric=True, launch_control=False, max_qubits=n)
+
+
+def _free_gib():
+    import torch
+
+    return torch.cuda.mem_get_info(0)[0] / 2**30
+
+
+def test_symmetric_n31_against_full():
+    """N=31 (odd: u3r(30) + isolated node): the 16 GiB half against the 32 GiB
+    full state, <C> and 64 sample blocks of 4096 amplitudes."""
+    if _free_gib() < 60:
+        pytest.skip("needs 60 GiB")
+    n = 31
+    g = Q.Graph.from_edges(n, list(Q.random_regular_graph(30, 3, seed=0).edges))
+    pr = Q.params_from_seed(3, 0)
+    offs = np.linspace(0, (1 << n) - 4096, 64).astype(np.int64) // 4096 * 4096
+    full = Q.simulate(g, pr, "bitwise", max_qubits=n)
+    e_full = Q.expectation(g, full)
+    blocks_full = np.concatenate([full.engine().read(int(o), 4096) for o in offs])
+    full.engine().close()
+    sym = Q.simulate(g, pr, "bitwise", symmetric=True, max_qubits=n)
+    h = 1 << (n - 1)
+    he = sym.half_engine
+    blocks = []
+    for o in offs:
+        o = int(o)
+        if o < h:
+            blocks.append(he.read(o, 4096))
+        else:  # psi(x) = psi(~x): the mirrored block of the half, reversed
+            lo = (1 << n) - 1 - (o + 4095)
+            blocks.append(he.read(lo, 4096)[::-1])
+    assert np.max(np.abs(np.concatenate(blocks) - blocks_full)) <= 1e-12
+    assert Q.expectation(g, sym) == pytest.approx(e_full, rel=1e-10)
+    he.close()
+
+
+def test_symmetric_n34_p1_closed_form():
+    """N=34 on ONE B200 (the half is 128 GiB; the full state would not fit):
+    p=1 per-edge closed form and the norm."""
+    if _free_gib() < 132:
+        pytest.skip("needs 132 GiB")
+    from oracle import oracle as O
+
+    g = Q.random_regular_graph(34, 3, seed=0)
+    gm, bt = O.params_from_seed(1, 0)
+    s = Q.simulate(g, Q.QaoaParams(gm, bt), "bitwise", symmetric=True, max_qubits=34)
+    try:
+        assert Q.expectation(g, s) == pytest.approx(16.931923255348405, rel=1e-10)
+        assert s.norm() == pytest.approx(1.0, abs=1e-12)
+    finally:
+        s.half_engine.close()
