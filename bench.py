@@ -683,6 +683,30 @@ def run_ours(args, rank: int, world: int, local: int):
                "steps": args.e2e_steps}
         assert abs(val - expect_val) <= 1e-10 * abs(expect_val)
 
+    # ---- symmetric half-state mode (opt-in API mode, NOT the headline): the
+    # same circuit on the 2^(N-1)-amplitude half, psi(x) == psi(~x) ----------
+    sym = None
+    if (args.symmetric_probe and world == 1 and n >= 13 and g.is_unweighted and not args.exact
+            and torch.cuda.mem_get_info(device)[0] > (16 << (n - 1)) + (4 << 30)):
+        from paper_2312_03019_b200.symmetric import simulate_symmetric
+
+        ss = simulate_symmetric(g, params)
+        for _ in range(max(args.warmup, 3) - 1):
+            simulate_symmetric(g, params, state=ss)
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            simulate_symmetric(g, params, state=ss)
+            e_sym = Q.expectation(g, ss)
+        sym_s = time.perf_counter() - t0
+        sym = {"value": p * args.steps / sym_s, "unit": UNIT, "ms_per_step": 1e3 * sym_s / args.steps,
+               "timing": "wall clock over K host-driven steps (segmented run + one mirror pass "
+                         "per level), <C> read back every step",
+               "state": f"2^{n - 1} amplitudes (the x_{n - 1} = 0 half; psi(x) == psi(~x) bit for "
+                        "bit), simulate(..., symmetric=True); not the headline",
+               "expectation": e_sym, "expectation_rel_diff": abs(e_sym - expect_val) / abs(expect_val)}
+        ss.half_engine.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -711,6 +735,7 @@ def run_ours(args, rank: int, world: int, local: int):
             "expectation": expect_val,
             "closed_form_p1": closed_form_check(g, params, expect_val),
             "cut_table_build": cut_table,
+            "symmetric_mode": sym,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -744,6 +769,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None,
                     help="end-to-end loop steps (default: --steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-symmetric-probe", dest="symmetric_probe", action="store_false",
+                    help="skip the symmetric half-state mode measurement (reported beside the "
+                         "headline, never as it)")
     ap.add_argument("--no-cut-table", dest="cut_table", action="store_false",
                     help="skip timing the K1 cut-table builder")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",

@@ -138,3 +138,16 @@ def test_oracle_single_gates_bit_exact(oracle):
         else:
             oracle.apply_rzz(a, n, op[1], op[2], op[3])
         assert np.array_equal(a, arrays[f"gate_out_{k}"]), op
+
+
+def test_reference_states_are_flip_symmetric(golden):
+    """The premise of the symmetric half-state mode, pinned on the REFERENCE's
+    own outputs: every launch-control state it produced satisfies
+    psi(x) == psi(~x) bit for bit (golden_small.npz, made by running it)."""
+    meta, arrays = golden
+    checked = 0
+    for case in meta["cases"]:
+        a = arrays["amps_" + case["name"]]
+        assert np.array_equal(a, a[::-1]), case["name"]
+        checked += 1
+    assert checked >= 20
