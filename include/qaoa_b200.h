@@ -43,9 +43,12 @@ extern "C" {
 #define QAOA_RUN_EXPECTATION 0x4    /* fuse <C> into the last sweep (qaoa_expectation)  */
 #define QAOA_RUN_TIMING 0x8         /* record per-launch CUDA-event times               */
 #define QAOA_RUN_SHARDED 0x10       /* qaoa_run_begin: exchange points after S_0 of every level */
-#define QAOA_RUN_MIRROR 0x40        /* with QAOA_RUN_SHARDED: exact runs put the exchange point
+#define QAOA_RUN_MIRROR 0x40        /* symmetric half state (graph of n_local + 1 nodes).
+                                       With QAOA_RUN_SHARDED: exact runs put the exchange point
                                        after the LAST qubit set of each level (the virtual top
-                                       qubit of a symmetric half state, qaoa_mirror_rx) */
+                                       qubit, qaoa_mirror_rx).  Without it (qaoa_run_layers, fast
+                                       schedule, n_local >= 22): every low-set sweep applies the
+                                       virtual top qubit's RX itself (2-CTA clusters) */
 #define QAOA_RUN_EXPECT_ONLY 0x20   /* with QAOA_RUN_EXPECTATION: the last sweep only reads (16 B
                                        instead of 32 B per amplitude); the state is left unusable
                                        (amplitude reads and QAOA_RUN_FROM_STATE then fail) */
@@ -118,7 +121,8 @@ QAOA_API int qaoa_apply_rx(qaoa_ctx* ctx, int qubit, double c, double s);
  * factor as returned by qaoa_run_exchange_info for the level) in one in-place
  * pass.  Driven by the host at the exchange points of a qaoa_run_begin(...,
  * QAOA_RUN_SHARDED | QAOA_RUN_MIRROR) run; <C> and the norm of the full state
- * are twice the half's. */
+ * are twice the half's.  Fast runs with n_local >= 22 need no host loop:
+ * qaoa_run_layers(..., QAOA_RUN_MIRROR) fuses the pass into the low-set sweeps. */
 QAOA_API int qaoa_mirror_rx(qaoa_ctx* ctx, const double* rx, const double* factor);
 
 /* Gate-level baseline (the reference's default backend "baseline" and

@@ -72,6 +72,9 @@ struct SweepPlan {
 struct RunState {
   bool active = false;
   bool exact = false, want_expect = false, timing = false, from_state = false, sharded = false;
+  // symmetric half state, fast schedule, one call: every low-set sweep also
+  // applies the virtual top qubit's RX (kMirror, 2-CTA clusters)
+  bool mirror_fused = false;
   int p = 0;
   std::vector<SetDesc> sets;
   std::vector<SweepPlan> plan;
@@ -346,7 +349,7 @@ void plan_swaps(qaoa_ctx* c, RunState& R) {
   R.lay.assign(R.plan.size(), 0);
   R.do_swap.assign(R.plan.size(), 0);
   const int ns = (int)R.sets.size();
-  if (R.exact || R.weighted || R.sharded || ns < 3 || c->swap_mode == 0) return;
+  if (R.exact || R.weighted || R.sharded || R.mirror_fused || ns < 3 || c->swap_mode == 0) return;
   if (c->swap_mode < 0) {
     static int env = -2;
     if (env == -2) {
@@ -497,6 +500,15 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
 
   R.sets = make_sets(n);
   R.plan = make_plan((int)R.sets.size(), p, R.exact, sharded, (flags & QAOA_RUN_MIRROR) != 0);
+  R.mirror_fused = (flags & QAOA_RUN_MIRROR) && !sharded;
+  if (R.mirror_fused && (R.exact || R.weighted || R.sets.size() < 3 || n_total != n + 1))
+    return fail(QAOA_E_INVALID,
+                "QAOA_RUN_MIRROR without QAOA_RUN_SHARDED is the fused fast schedule: it needs a "
+                "graph of n_local + 1 nodes, n_local >= 22 and no QAOA_RUN_EXACT (use the "
+                "segmented run with qaoa_mirror_rx otherwise)");
+  // per-qubit RX factors of a level: the local qubits, plus the virtual top one
+  // when its RX is fused into the low-set sweeps
+  const int n_rx = n + (R.mirror_fused ? 1 : 0);
 
   // phase tables: the sweeps only index even entries (t = E - 2C), so upload
   // table_even[k] = table[2k], k = 0..E.  exact = as given; fast = scaled by
@@ -525,13 +537,13 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
       // RX = c [[1, -i t], [-i t, 1]], t = s / c
       R.stages[l] = RxStage{sn[l] / cs[l], 0.0, 1};
       R.level_factor[l] = std::complex<double>(cs[l], 0.0);
-      prev_scale = std::pow(R.level_factor[l], n);
+      prev_scale = std::pow(R.level_factor[l], n_rx);
     } else {
       // RX = (-i s) X [[1, i k], [i k, 1]], k = c / s: run form 1 with t = -k and
       // complement every bit (X^n) by bookkeeping instead of data movement.
       R.stages[l] = RxStage{-cs[l] / sn[l], 0.0, 1};
       R.level_factor[l] = std::complex<double>(0.0, -sn[l]);
-      prev_scale = std::pow(R.level_factor[l], n);
+      prev_scale = std::pow(R.level_factor[l], n_rx);
       R.flips ^= 1;
     }
   }
@@ -665,6 +677,8 @@ int launch_plan_sweep(qaoa_ctx* c, int i, int64_t lo, int64_t cnt) {
   if (sp.stage1 >= 0) {
     fl |= kStage1;
     a.rx1 = R.stages[sp.stage1];
+    // the low set is a single-stage middle sweep of every level in these plans
+    if (R.mirror_fused && sp.set == 0) fl |= kMirror;
   }
   if (sp.stage2 >= 0) {
     fl |= kStage2;
@@ -724,8 +738,10 @@ int run_end(qaoa_ctx* c) {
   if (R.flips) {
     // sharded: complement all n_nodes bits (C(x) = C(~x) keeps the cost kernels
     // exact with the run's initial mask); unsharded: all local bits = all bits
-    const uint64_t all = R.sharded ? (c->g.n_nodes >= 64 ? ~0ull : ((1ull << c->g.n_nodes) - 1ull))
-                                   : local_mask(c);
+    // (a fused symmetric run: all n_local + 1 bits, X^N is the identity there)
+    const uint64_t all = (R.sharded || R.mirror_fused)
+                             ? (c->g.n_nodes >= 64 ? ~0ull : ((1ull << c->g.n_nodes) - 1ull))
+                             : local_mask(c);
     c->g.cmask ^= all;
   }
   if (R.expect_fused) {

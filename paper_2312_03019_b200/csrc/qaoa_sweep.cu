@@ -41,7 +41,36 @@ namespace qb {
 // One 4096-amplitude tile per CTA; two CTAs per SM keep one tile's loads in
 // flight while the other computes (a persistent grid measured slower).
 // WGT: weighted cost (fast flows only; wbasis / apply_wcost in qaoa_tile.cuh).
-template <bool WIDE, int C, int FLOW, bool WGT = false>
+//
+// MIR (symmetric half state, low set, fast flow 1, launched as clusters of two
+// CTAs): RX on the virtual top qubit N-1 after the set's RX stage.  The half
+// state holds psi(x) for x_{N-1} = 0 and psi(x) == psi(~x), so that qubit pairs
+// stored index y with y ^ (2^n - 1): element i of tile T with element 4095 - i
+// of tile ~T.  Cluster pair k runs tile k (rank 0) and tile ntiles - 1 - k
+// (rank 1); both publish their finished tile in their own exchange buffer,
+// and after one cluster barrier each CTA takes half of the 4096 pairs (own
+// elements i < 2048 with the partner's 4095 - i, read over DSMEM) and stores
+// both outputs of each pair -- 32 KB per CTA cross the cluster.  This replaces
+// the separate mirror pass (one more HBM round trip of the half state) of the
+// segmented schedule.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ double2 ld_dsmem(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+
+template <bool WIDE, int C, int FLOW, bool WGT = false, bool MIR = false>
 __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constant__ SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);  // kSlots exchange slots
@@ -62,6 +91,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   // vary the low bits of BOTH swapped ranges, so the tiles in flight share a
   // few DRAM pages on the read side and on the write side
   auto visit = [&](uint64_t b) -> uint64_t {
+    if (MIR) return (b & 1ull) ? (uint64_t)a.ntiles - 1ull - (b >> 1) : (b >> 1);
     if (C < 12 || !a.out) return b;
     const int k = a.sw_m / 2 < 4 ? a.sw_m / 2 : 4;
     return swap_bit_ranges(b, k, a.sw_hi - 12, k);
@@ -159,7 +189,40 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     constexpr int last = fast_last<C, FLOW>();
     if (flags & kExpect)
       acc = WGT ? expect_wacc<last>(v, &wcb[0], a.wc, tid, sk) : expect_acc<last>(v, &cb, tid, sk);
-    if (C >= 12 && a.out) {  // out of place into the swapped qubit layout
+    if (MIR) {
+      // publish the finished tile (the slots this thread read in the last
+      // exchange: no CTA-internal hazard), then pairs (i, 4095 - i) across the
+      // cluster; this CTA's tile is `tile`, the partner's ntiles - 1 - tile
+      smem_store<last>(buf, ts.s[last], v);
+      cluster_arrive();
+      cluster_wait();
+      const uint32_t lb = (uint32_t)__cvta_generic_to_shared(buf);
+      uint32_t rb;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(cluster_rank() ^ 1u));
+      double2 own[kRegs / 2], par[kRegs / 2];
+#pragma unroll
+      for (int k = 0; k < kRegs / 2; ++k) {
+        const int i = tid + kThreads * k;  // own element, i < 2048
+        own[k] = buf[slot(i)];
+        par[k] = ld_dsmem(rb + 16u * (uint32_t)slot(kTile - 1 - i));
+      }
+      cluster_arrive();  // done with the partner's buffer
+      const double t = a.rx1.a;
+      double2* po = amps + (tile << 12);
+      double2* pp = amps + (((uint64_t)a.ntiles - 1ull - tile) << 12) + (kTile - 1);
+#pragma unroll
+      for (int k = 0; k < kRegs / 2; ++k) {
+        const int i = tid + kThreads * k;
+        rx_form1(own[k], par[k], t);
+        if (flags & kScale) {
+          own[k] = cmul_np(own[k], a.scale);
+          par[k] = cmul_np(par[k], a.scale);
+        }
+        __stcs(po + i, own[k]);
+        __stcs(pp - i, par[k]);
+      }
+      cluster_wait();  // the partner is done with this CTA's buffer before it exits
+    } else if (C >= 12 && a.out) {  // out of place into the swapped qubit layout
       TileCtx to = tc;
       to.base = swap_bit_ranges(tc.base, a.sw_lo, a.sw_hi, a.sw_m);
       store_tile<C, last>(a.out, to, Q, v, flags, sk);
@@ -246,6 +309,37 @@ static cudaError_t launch_one(const SweepArgs& a, int grid, size_t smem, cudaStr
   return cudaGetLastError();
 }
 
+// Low-set sweep with the virtual top qubit's RX (kMirror): clusters of two CTAs.
+template <bool WIDE>
+static cudaError_t launch_mirror(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {
+  if (a.carry != 12 || (a.flags & (kExact | kWeighted | kStage2 | kExpect | kNoStore | kGen)) || a.out ||
+      a.tile_lo != 0 || (a.tile_cnt && a.tile_cnt != a.ntiles) || a.ntiles < 2 || (grid & 1))
+    return cudaErrorInvalidValue;
+  static unsigned long long configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  auto kern = sweep_kernel<WIDE, 12, 1, false, true>;
+  if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
 template <bool WIDE, int C>
 static cudaError_t launch_c(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {
   if (a.flags & kExact) return launch_one<WIDE, C, 0>(a, grid, smem, s);
@@ -259,6 +353,7 @@ static cudaError_t launch_c(const SweepArgs& a, int grid, size_t smem, cudaStrea
 
 template <bool WIDE>
 static cudaError_t launch_w(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {
+  if (a.flags & kMirror) return launch_mirror<WIDE>(a, grid, smem, s);
   switch (a.carry) {
     case 3: return launch_c<WIDE, 3>(a, grid, smem, s);
     case 4: return launch_c<WIDE, 4>(a, grid, smem, s);

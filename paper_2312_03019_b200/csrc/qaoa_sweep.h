@@ -19,6 +19,8 @@ enum SweepFlags : uint32_t {
   kExact = 1u << 7,    // reference arithmetic + increasing qubit order
   kNoStore = 1u << 8,  // read-only sweep
   kWeighted = 1u << 9, // weighted cost: factored per-edge phases (see apply_wcost)
+  kMirror = 1u << 10,  // symmetric half state: RX on the virtual top qubit after the
+                       // stage (pairs tile T with tile ~T, a 2-CTA cluster; see qaoa_sweep.cu)
 };
 
 struct SweepArgs {

@@ -441,7 +441,7 @@ void set_sweep_impl(int v) { g_impl = v; }
 //   at N=33 the C = 5 top set is faster one tile per CTA: 50.1 vs 53.1 ms)
 //   everything else                  v4 + L2 prefetch is fastest        -> 0
 int sweep_impl(const SweepArgs& a) {
-  if ((a.flags & (kExact | kWeighted)) || a.carry == 11 || a.ntiles < 1 || a.out) return 0;
+  if ((a.flags & (kExact | kWeighted | kMirror)) || a.carry == 11 || a.ntiles < 1 || a.out) return 0;
   const int env = impl_env();
   if (env != 3) return env;
   if (a.flags & kGen) return 2;

@@ -10,16 +10,20 @@ MaxCut QAOA keeps the state invariant under the global bit flip X^N:
 The engine therefore stores only the half with the top qubit N-1 = 0: a
 context of N-1 local qubits whose graph has N nodes (the top node is a fixed
 0 bit, like the shard bits of a sharded state).  RX on the top qubit pairs
-stored y with y ^ (2^(N-1) - 1) (`qaoa_mirror_rx`, one in-place pass), run
-at the exchange points of a segmented run (`qaoa_run_begin(...,
-QAOA_RUN_SHARDED | QAOA_RUN_MIRROR)`): after S_0 in the fast schedule, after
-the level's last set in the exact one (the reference applies qubit N-1
-last).  <C> and the norm of the full state are twice the half's.  Every
-amplitude of the full state is available (`.amps` mirrors the half).
+stored y with y ^ (2^(N-1) - 1).  Fast runs with N-1 >= 22 apply it inside
+every low-set sweep (`qaoa_run_layers(..., QAOA_RUN_MIRROR)`: tile T and
+tile ~T run in one 2-CTA cluster and trade halves over distributed shared
+memory), so a level costs the sweeps of a full state of half the size.  Exact
+runs (and N-1 < 22) use one in-place pass (`qaoa_mirror_rx`) at the exchange
+points of a segmented run (`qaoa_run_begin(..., QAOA_RUN_SHARDED |
+QAOA_RUN_MIRROR)`): after S_0 in the fast schedule, after the level's last
+set in the exact one (the reference applies qubit N-1 last).  <C> and the
+norm of the full state are twice the half's.  Every amplitude of the full
+state is available (`.amps` mirrors the half).
 
-Half the HBM bytes and half the arithmetic per level, plus one mirror pass
-of the half state per level; N=34 fits one B200.  Opt-in
-(``simulate(..., symmetric=True)``); unweighted graphs with launch control.
+Half the HBM bytes and half the arithmetic per level; N=34 fits one B200.
+Opt-in (``simulate(..., symmetric=True)``); unweighted graphs with launch
+control.
 """
 
 from __future__ import annotations
@@ -108,6 +112,12 @@ class SymmetricState(StateVector):
         return 2.0 * he.scalar("qaoa_expectation")
 
 
+# Fast runs with at least this many local qubits (three or more qubit sets,
+# so the low set is always a single-stage middle sweep) run in one
+# qaoa_run_layers call with the mirror fused into the low-set sweeps.
+FUSED_MIN_LOCAL = 22
+
+
 def _normalize_top_bit(eng: Engine) -> None:
     """A complement mask with the virtual top bit set describes the same
     stored data as the mask with every bit flipped (psi(x) == psi(~x)): keep
@@ -121,8 +131,10 @@ def _normalize_top_bit(eng: Engine) -> None:
 
 def simulate_symmetric(g: Graph, params, exact: bool = False, fuse_expectation: bool = True,
                        state: SymmetricState | None = None, device: int = 0,
-                       timing: bool = False) -> SymmetricState:
-    """The p-level circuit on the x_{N-1} = 0 half of the state (see module doc)."""
+                       timing: bool = False, fused: bool | None = None) -> SymmetricState:
+    """The p-level circuit on the x_{N-1} = 0 half of the state (see module doc).
+    ``fused``: None picks the one-call schedule whenever it applies (fast, N-1 >=
+    22); False forces the segmented run with separate mirror passes."""
     from .circuit import level_arrays
 
     n = g.n
@@ -130,11 +142,22 @@ def simulate_symmetric(g: Graph, params, exact: bool = False, fuse_expectation: 
         raise ValueError("the symmetric half-state mode needs at least 13 qubits")
     if not g.is_unweighted:
         raise ValueError("the symmetric half-state mode runs unweighted graphs")
+    if fused is None:
+        fused = not exact and n - 1 >= FUSED_MIN_LOCAL
+    if fused and (exact or n - 1 < FUSED_MIN_LOCAL):
+        raise ValueError("the fused symmetric schedule is fast-mode with N >= 23")
     he = state.half_engine if isinstance(state, SymmetricState) and state.n == n else None
     eng = he if he is not None else Engine(n - 1, device)
     eng.ensure_graph(g)
     tables, cs, ss = level_arrays(g, params)
     t = np.ascontiguousarray(tables)
+    if fused:
+        # one call: the low-set sweeps apply the top qubit's RX themselves
+        flags = _lib.RUN_MIRROR | (_lib.RUN_EXPECTATION if fuse_expectation else 0) | \
+            (_lib.RUN_TIMING if timing else 0)
+        eng.call("qaoa_run_layers", params.p, _lib.dptr(t.view(np.float64)), _lib.dptr(cs),
+                 _lib.dptr(ss), flags)
+        return _finish(eng, g, params, state, he)
     flags = _lib.RUN_SHARDED | _lib.RUN_MIRROR | (_lib.RUN_EXACT if exact else 0) | \
         (_lib.RUN_EXPECTATION if fuse_expectation else 0) | (_lib.RUN_TIMING if timing else 0)
     nseg = ctypes.c_int()
@@ -152,6 +175,11 @@ def simulate_symmetric(g: Graph, params, exact: bool = False, fuse_expectation: 
         _lib.check(rc)
         eng.call("qaoa_mirror_rx", _lib.dptr(rx), _lib.dptr(factor))
     eng.call("qaoa_run_end")
+    return _finish(eng, g, params, state, he)
+
+
+def _finish(eng: Engine, g: Graph, params, state, he) -> SymmetricState:
+    n = g.n
     _normalize_top_bit(eng)
     write_counter.add((1 << n) * (1 + params.p * (n + 1)))
     if state is not None and isinstance(state, SymmetricState) and he is not None:

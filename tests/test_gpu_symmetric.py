@@ -127,3 +127,55 @@ def test_symmetric_n34_p1_closed_form():
         assert s.norm() == pytest.approx(1.0, abs=1e-12)
     finally:
         s.half_engine.close()
+
+
+@pytest.mark.parametrize("n,betas", [
+    (23, (0.4, 1.1, 2.0)),          # 22 local qubits: the smallest fused case
+    (25, (0.3, 2.9, 1.0, 2.7)),     # odd: u3r(24) + isolated node; second-form levels
+    (26, (2.95, 0.2, 3.05, 1.4, 0.6)),
+])
+def test_fused_mirror_matches_segmented_and_oracle(oracle, n, betas):
+    """The low-set sweeps with the top qubit's RX fused (2-CTA clusters over
+    DSMEM, one qaoa_run_layers call) against the segmented run (one mirror pass
+    per level) and the oracle's full state: amplitudes within 1e-12, <C> 1e-10."""
+    from paper_2312_03019_b200.symmetric import simulate_symmetric
+
+    g = Q.random_regular_graph(n, 3, seed=n) if n % 2 == 0 else \
+        Q.Graph.from_edges(n, list(Q.random_regular_graph(n - 1, 3, seed=n).edges))
+    gammas = tuple(0.3 + 0.7 * k for k in range(len(betas)))
+    pr = Q.QaoaParams(gammas, betas)
+    ref = oracle.simulate(n, g.row_mask, g.tot_edge, gammas, betas)
+    eref = oracle.expectation(n, g.row_mask, ref)
+    fu = simulate_symmetric(g, pr, fused=True)
+    seg = simulate_symmetric(g, pr, fused=False)
+    e_fu, e_seg = fu.expectation(g), seg.expectation(g)
+    assert e_fu == pytest.approx(eref, rel=1e-10) and e_seg == pytest.approx(eref, rel=1e-10)
+    a_fu, a_seg = fu.amps, seg.amps
+    assert np.max(np.abs(a_fu - ref)) <= 1e-12
+    assert np.max(np.abs(a_fu - a_seg)) <= 1e-13
+    assert fu.norm() == pytest.approx(1.0, abs=1e-12)
+
+
+def test_fused_mirror_refusals():
+    """QAOA_RUN_MIRROR without QAOA_RUN_SHARDED: fast schedule, n_local >= 22,
+    a graph of n_local + 1 nodes; anything else is refused with a message."""
+    from paper_2312_03019_b200 import _lib
+    from paper_2312_03019_b200.circuit import level_arrays
+    from paper_2312_03019_b200.symmetric import simulate_symmetric
+
+    pr = Q.params_from_seed(2, 0)
+    g = Q.random_regular_graph(22, 3, seed=1)
+    with pytest.raises(ValueError, match="fused"):
+        simulate_symmetric(g, pr, fused=True)  # 21 local qubits
+    g24 = Q.random_regular_graph(24, 3, seed=1)
+    with pytest.raises(ValueError, match="fused"):
+        simulate_symmetric(g24, pr, exact=True, fused=True)
+    eng = Q.Engine(23)
+    try:
+        eng.ensure_graph(Q.random_regular_graph(22, 3, seed=1))  # n_local + 1 != nodes
+        tables, cs, ss = level_arrays(Q.random_regular_graph(22, 3, seed=1), pr)
+        with pytest.raises(ValueError, match="n_local \\+ 1"):
+            eng.call("qaoa_run_layers", 2, _lib.dptr(np.ascontiguousarray(tables).view(np.float64)),
+                     _lib.dptr(cs), _lib.dptr(ss), _lib.RUN_MIRROR)
+    finally:
+        eng.close()
