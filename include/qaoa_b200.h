@@ -47,8 +47,8 @@ extern "C" {
                                        With QAOA_RUN_SHARDED: exact runs put the exchange point
                                        after the LAST qubit set of each level (the virtual top
                                        qubit, qaoa_mirror_rx).  Without it (qaoa_run_layers, fast
-                                       schedule, n_local >= 22): every low-set sweep applies the
-                                       virtual top qubit's RX itself (2-CTA clusters) */
+                                       schedule): the low set becomes the mirror low set, local
+                                       qubits 0..10 plus the virtual top qubit in one sweep */
 #define QAOA_RUN_EXPECT_ONLY 0x20   /* with QAOA_RUN_EXPECTATION: the last sweep only reads (16 B
                                        instead of 32 B per amplitude); the state is left unusable
                                        (amplitude reads and QAOA_RUN_FROM_STATE then fail) */
@@ -121,8 +121,9 @@ QAOA_API int qaoa_apply_rx(qaoa_ctx* ctx, int qubit, double c, double s);
  * factor as returned by qaoa_run_exchange_info for the level) in one in-place
  * pass.  Driven by the host at the exchange points of a qaoa_run_begin(...,
  * QAOA_RUN_SHARDED | QAOA_RUN_MIRROR) run; <C> and the norm of the full state
- * are twice the half's.  Fast runs with n_local >= 22 need no host loop:
- * qaoa_run_layers(..., QAOA_RUN_MIRROR) fuses the pass into the low-set sweeps. */
+ * are twice the half's.  Fast runs need no host loop and no extra pass:
+ * qaoa_run_layers(..., QAOA_RUN_MIRROR) folds the virtual qubit into the low-set
+ * sweeps (tile = stored block u plus block ~u read backwards). */
 QAOA_API int qaoa_mirror_rx(qaoa_ctx* ctx, const double* rx, const double* factor);
 
 /* Gate-level baseline (the reference's default backend "baseline" and

@@ -200,10 +200,14 @@ int ensure_tables(qaoa_ctx* c, size_t n) {
   return QAOA_OK;
 }
 
-std::vector<SetDesc> make_sets(int n) {
+// mirror: a symmetric half state's fused schedule -- set 0 is the mirror low
+// set (local qubits 0..10 plus the virtual top qubit n, SetDesc{12, n}; see
+// sweep_kernel's MIR) and the high sets cover local qubits 11..n-1.
+std::vector<SetDesc> make_sets(int n, bool mirror = false) {
   std::vector<SetDesc> sets;
-  sets.push_back(SetDesc{12, 0});
-  const int rem = n - 12;
+  sets.push_back(SetDesc{12, mirror ? n : 0});
+  const int first = mirror ? 11 : 12;
+  const int rem = n - first;
   if (rem <= 0) return sets;
   const int chunks = (rem + 8) / 9;  // at most 9 mixed bits per high sweep (C >= 3)
   // the r = rem % chunks extra bits go to the middle chunks first, the ends
@@ -222,7 +226,7 @@ std::vector<SetDesc> make_sets(int n) {
       ++size[chunks - 1];
     }
   }
-  int next = 12;
+  int next = first;
   for (int ci = 0; ci < chunks; ++ci) {
     sets.push_back(SetDesc{12 - size[ci], next});
     next += size[ci];
@@ -498,14 +502,14 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
     return fail(QAOA_E_STATE, "the state was not stored by the last run (QAOA_RUN_EXPECT_ONLY)");
   if (!R.from_state) c->g.cmask = 0;
 
-  R.sets = make_sets(n);
-  R.plan = make_plan((int)R.sets.size(), p, R.exact, sharded, (flags & QAOA_RUN_MIRROR) != 0);
   R.mirror_fused = (flags & QAOA_RUN_MIRROR) && !sharded;
-  if (R.mirror_fused && (R.exact || R.weighted || R.sets.size() < 3 || n_total != n + 1))
+  if (R.mirror_fused && (R.exact || R.weighted || n_total != n + 1))
     return fail(QAOA_E_INVALID,
                 "QAOA_RUN_MIRROR without QAOA_RUN_SHARDED is the fused fast schedule: it needs a "
-                "graph of n_local + 1 nodes, n_local >= 22 and no QAOA_RUN_EXACT (use the "
-                "segmented run with qaoa_mirror_rx otherwise)");
+                "graph of n_local + 1 nodes and no QAOA_RUN_EXACT (use the segmented run with "
+                "qaoa_mirror_rx otherwise)");
+  R.sets = make_sets(n, R.mirror_fused);
+  R.plan = make_plan((int)R.sets.size(), p, R.exact, sharded, (flags & QAOA_RUN_MIRROR) != 0);
   // per-qubit RX factors of a level: the local qubits, plus the virtual top one
   // when its RX is fused into the low-set sweeps
   const int n_rx = n + (R.mirror_fused ? 1 : 0);
@@ -677,9 +681,8 @@ int launch_plan_sweep(qaoa_ctx* c, int i, int64_t lo, int64_t cnt) {
   if (sp.stage1 >= 0) {
     fl |= kStage1;
     a.rx1 = R.stages[sp.stage1];
-    // the low set is a single-stage middle sweep of every level in these plans
-    if (R.mirror_fused && sp.set == 0) fl |= kMirror;
   }
+  if (R.mirror_fused && sp.set == 0) fl |= kMirror;  // the mirror low set
   if (sp.stage2 >= 0) {
     fl |= kStage2;
     a.rx2 = R.stages[sp.stage2];

@@ -42,32 +42,27 @@ namespace qb {
 // flight while the other computes (a persistent grid measured slower).
 // WGT: weighted cost (fast flows only; wbasis / apply_wcost in qaoa_tile.cuh).
 //
-// MIR (symmetric half state, low set, fast flow 1, launched as clusters of two
-// CTAs): RX on the virtual top qubit N-1 after the set's RX stage.  The half
-// state holds psi(x) for x_{N-1} = 0 and psi(x) == psi(~x), so that qubit pairs
-// stored index y with y ^ (2^n - 1): element i of tile T with element 4095 - i
-// of tile ~T.  Cluster pair k runs tile k (rank 0) and tile ntiles - 1 - k
-// (rank 1); both publish their finished tile in their own exchange buffer,
-// and after one cluster barrier each CTA takes half of the 4096 pairs (own
-// elements i < 2048 with the partner's 4095 - i, read over DSMEM) and stores
-// both outputs of each pair -- 32 KB per CTA cross the cluster.  This replaces
-// the separate mirror pass (one more HBM round trip of the half state) of the
-// segmented schedule.
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_arrive() {
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ double2 ld_dsmem(uint32_t addr) {
-  double2 v;
-  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
-  return v;
+// MIR (symmetric half state, fast flow 1): the "mirror low set".  The half
+// state of an N = n + 1 qubit state stores psi(v) for v_n = 0 (psi(v) ==
+// psi(~v)), so virtual index v lives at fold(v) = v_n ? ~v : v (n bits).  A
+// mirror tile u (u < 2^(n-12)) is the virtual tile with bits 0..10 and the
+// virtual top bit n: tile index t < 2048 is stored block u (2048 contiguous
+// amplitudes, ascending), t >= 2048 is block 2^(n-11) - 1 - u read backwards
+// (fold).  So one sweep mixes qubits 0..10 AND the virtual top qubit (tile bit
+// 11) with two contiguous 32 KB runs per tile and no cross-CTA traffic; the
+// cost geometry is the standard (C = 11, q = n) one in virtual coordinates
+// (C(v) = C(~v)).  The planner gives the high sets qubits 11..n-1.
+template <int M>
+__device__ __forceinline__ void mirror_ptrs(double2* amps, uint64_t u, uint64_t nblocks, int tid,
+                                            double2* (&ptr)[kRegs]) {
+  double2* const b1 = amps + (u << 11);                                  // t < 2048: b1 + t
+  double2* const b2 = amps + ((nblocks - 1ull - u) << 11) + 2047;        // t >= 2048: b2 - (t - 2048)
+  const int tp = tile_index<M>(tid, 0);
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    const int t = tp | tile_index<M>(0, r);  // disjoint bit parts
+    ptr[r] = (t & 2048) ? b2 - (t & 2047) : b1 + t;
+  }
 }
 
 template <bool WIDE, int C, int FLOW, bool WGT = false, bool MIR = false>
@@ -91,7 +86,6 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   // vary the low bits of BOTH swapped ranges, so the tiles in flight share a
   // few DRAM pages on the read side and on the write side
   auto visit = [&](uint64_t b) -> uint64_t {
-    if (MIR) return (b & 1ull) ? (uint64_t)a.ntiles - 1ull - (b >> 1) : (b >> 1);
     if (C < 12 || !a.out) return b;
     const int k = a.sw_m / 2 < 4 ? a.sw_m / 2 : 4;
     return swap_bit_ranges(b, k, a.sw_hi - 12, k);
@@ -100,8 +94,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   TileCtx tc;
   {
     const int low_bits = C >= 12 ? 0 : q - C;  // non-tile ranges [C, q) and [q + 12 - C, n)
-    tc.base = C >= 12 ? (tile << 12)
-                      : (((tile & ((1ull << low_bits) - 1ull)) << C) | ((tile >> low_bits) << (q + 12 - C)));
+    tc.base = MIR ? (tile << 11)  // virtual index of tile element 0 (bits 0..10 and n clear)
+                  : C >= 12 ? (tile << 12)
+                  : (((tile & ((1ull << low_bits) - 1ull)) << C) | ((tile >> low_bits) << (q + 12 - C)));
   }
   tc.tb2 = tile_off<C>(tile_index<2>(tid, 0), Q);
   tc.tb1 = tile_off<C>(tile_index<1>(tid, 0), Q);
@@ -121,7 +116,13 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     const uint64_t pf_b = (uint64_t)a.tile_lo + blockIdx.x + a.pf_dist;
     if (a.pf_dist > 0 && pf_b < (uint64_t)(a.tile_lo + (a.tile_cnt ? a.tile_cnt : a.ntiles))) {
       const uint64_t pf_tile = visit(pf_b);
-      if (!a.pf_tensor) {
+      if (MIR) {
+        if (tid < 2) {
+          const uint64_t blk = tid ? 2ull * (uint64_t)a.ntiles - 1ull - pf_tile : pf_tile;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(amps + (blk << 11)), "r"(32768u)
+                       : "memory");
+        }
+      } else if (!a.pf_tensor) {
         prefetch_tile_l2<C, kThreads>(amps, tile_base<C>(pf_tile, q), Q, tid);
       } else if (tid == 0) {
 #pragma unroll
@@ -135,7 +136,14 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         }
       }
     }
-    walk_tile<C, 2>(amps + tc.base + tc.tb2, Q, sk, [&](int r, double2* ptr) { v[r] = ld_tile(ptr); });
+    if (MIR) {
+      double2* ptr[kRegs];
+      mirror_ptrs<2>(amps, tile, 2ull * (uint64_t)a.ntiles, tid, ptr);
+#pragma unroll
+      for (int r = 0; r < kRegs; ++r) v[r] = ld_tile(ptr[r]);
+    } else {
+      walk_tile<C, 2>(amps + tc.base + tc.tb2, Q, sk, [&](int r, double2* ptr) { v[r] = ld_tile(ptr); });
+    }
   }
   const bool need_cut = flags & (kPreCost | kMidCost | kExpect);
   if (need_cut) {
@@ -145,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         if (flags & kMidCost) wbasis<C>(a, tc.base, q, a.wu2, &wb[WGT ? 1 : 0]);
       }
       if (WGT && (flags & kExpect)) wcut_basis<C>(a, tc.base, q, &wcb[0]);
-      if (!WGT) cut_basis<WIDE, C>(a, tc.base, q, &cb);
+      if (!WGT) cut_basis<WIDE, MIR ? 11 : C>(a, tc.base, q, &cb);  // MIR: q = n (virtual bit)
     }
     // The basis is first read after the fast flow's first register exchange
     // (whose barrier then publishes it) unless a cost step precedes every
@@ -190,38 +198,12 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     if (flags & kExpect)
       acc = WGT ? expect_wacc<last>(v, &wcb[0], a.wc, tid, sk) : expect_acc<last>(v, &cb, tid, sk);
     if (MIR) {
-      // publish the finished tile (the slots this thread read in the last
-      // exchange: no CTA-internal hazard), then pairs (i, 4095 - i) across the
-      // cluster; this CTA's tile is `tile`, the partner's ntiles - 1 - tile
-      smem_store<last>(buf, ts.s[last], v);
-      cluster_arrive();
-      cluster_wait();
-      const uint32_t lb = (uint32_t)__cvta_generic_to_shared(buf);
-      uint32_t rb;
-      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(cluster_rank() ^ 1u));
-      double2 own[kRegs / 2], par[kRegs / 2];
+      if (!(flags & kNoStore)) {
+        double2* ptr[kRegs];
+        mirror_ptrs<last>(amps, tile, 2ull * (uint64_t)a.ntiles, tid, ptr);
 #pragma unroll
-      for (int k = 0; k < kRegs / 2; ++k) {
-        const int i = tid + kThreads * k;  // own element, i < 2048
-        own[k] = buf[slot(i)];
-        par[k] = ld_dsmem(rb + 16u * (uint32_t)slot(kTile - 1 - i));
+        for (int r = 0; r < kRegs; ++r) __stcs(ptr[r], v[r]);
       }
-      cluster_arrive();  // done with the partner's buffer
-      const double t = a.rx1.a;
-      double2* po = amps + (tile << 12);
-      double2* pp = amps + (((uint64_t)a.ntiles - 1ull - tile) << 12) + (kTile - 1);
-#pragma unroll
-      for (int k = 0; k < kRegs / 2; ++k) {
-        const int i = tid + kThreads * k;
-        rx_form1(own[k], par[k], t);
-        if (flags & kScale) {
-          own[k] = cmul_np(own[k], a.scale);
-          par[k] = cmul_np(par[k], a.scale);
-        }
-        __stcs(po + i, own[k]);
-        __stcs(pp - i, par[k]);
-      }
-      cluster_wait();  // the partner is done with this CTA's buffer before it exits
     } else if (C >= 12 && a.out) {  // out of place into the swapped qubit layout
       TileCtx to = tc;
       to.base = swap_bit_ranges(tc.base, a.sw_lo, a.sw_hi, a.sw_m);
@@ -293,51 +275,29 @@ cudaError_t launch_wc_table(double* c_out, const int2* wedge, const double* w, i
 
 size_t sweep_smem_bytes(int) { return (size_t)kSlots * sizeof(double2); }
 
-template <bool WIDE, int C, int FLOW, bool WGT = false>
+template <bool WIDE, int C, int FLOW, bool WGT = false, bool MIR = false>
 static cudaError_t launch_one(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {
   static unsigned long long configured = 0;  // per instantiation, bit d = device d done
   int dev = 0;
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<WIDE, C, FLOW, WGT>,
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<WIDE, C, FLOW, WGT, MIR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
   }
-  sweep_kernel<WIDE, C, FLOW, WGT><<<grid, kThreads, smem, s>>>(a);
+  sweep_kernel<WIDE, C, FLOW, WGT, MIR><<<grid, kThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 
-// Low-set sweep with the virtual top qubit's RX (kMirror): clusters of two CTAs.
+// Mirror low set of a symmetric half state (kMirror, see sweep_kernel).
 template <bool WIDE>
 static cudaError_t launch_mirror(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {
-  if (a.carry != 12 || (a.flags & (kExact | kWeighted | kStage2 | kExpect | kNoStore | kGen)) || a.out ||
-      a.tile_lo != 0 || (a.tile_cnt && a.tile_cnt != a.ntiles) || a.ntiles < 2 || (grid & 1))
+  if (a.carry != 12 || (a.flags & (kExact | kWeighted)) || a.out || a.ntiles < 1)
     return cudaErrorInvalidValue;
-  static unsigned long long configured = 0;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const unsigned long long bit = 1ull << (dev & 63);
-  auto kern = sweep_kernel<WIDE, 12, 1, false, true>;
-  if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a);
+  if (a.flags & kStage2) return launch_one<WIDE, 12, 2, false, true>(a, grid, smem, s);
+  return launch_one<WIDE, 12, 1, false, true>(a, grid, smem, s);
 }
 
 template <bool WIDE, int C>
@@ -413,8 +373,8 @@ cudaError_t launch_sweep(const SweepArgs& a0, int grid, cudaStream_t stream) {
       const char* e = getenv("QAOA_PF_TENSOR");
       tens = e ? atoi(e) : 1;
     }
-    a.pf_tensor = tens;
-    if (tens) {
+    a.pf_tensor = (a.flags & kMirror) ? 0 : tens;  // mirror tiles: two per-run bulk prefetches
+    if (a.pf_tensor) {
       int n = 12;
       while ((1ll << (n - 12)) < a.ntiles) ++n;
       if (!make_tile_map(&a.map, a.amps, n, a.carry, a.q)) return cudaErrorInvalidValue;

@@ -10,14 +10,14 @@ MaxCut QAOA keeps the state invariant under the global bit flip X^N:
 The engine therefore stores only the half with the top qubit N-1 = 0: a
 context of N-1 local qubits whose graph has N nodes (the top node is a fixed
 0 bit, like the shard bits of a sharded state).  RX on the top qubit pairs
-stored y with y ^ (2^(N-1) - 1).  Fast runs with N-1 >= 22 apply it inside
-every low-set sweep (`qaoa_run_layers(..., QAOA_RUN_MIRROR)`: tile T and
-tile ~T run in one 2-CTA cluster and trade halves over distributed shared
-memory), so a level costs the sweeps of a full state of half the size.  Exact
-runs (and N-1 < 22) use one in-place pass (`qaoa_mirror_rx`) at the exchange
-points of a segmented run (`qaoa_run_begin(..., QAOA_RUN_SHARDED |
-QAOA_RUN_MIRROR)`): after S_0 in the fast schedule, after the level's last
-set in the exact one (the reference applies qubit N-1 last).  <C> and the
+stored y with y ^ (2^(N-1) - 1).  Fast runs fold it into the low-set sweep
+(`qaoa_run_layers(..., QAOA_RUN_MIRROR)`): a "mirror tile" is stored block u
+of 2048 amplitudes plus block ~u read backwards, i.e. the virtual tile of
+qubits 0..10 and N-1, so one sweep mixes both and the high sets take qubits
+11..N-2; a level costs the sweeps of a full state of half the size.  Exact
+runs use one in-place pass (`qaoa_mirror_rx`) at the exchange points of a
+segmented run (`qaoa_run_begin(..., QAOA_RUN_SHARDED | QAOA_RUN_MIRROR)`),
+after the level's last set (the reference applies qubit N-1 last).  <C> and the
 norm of the full state are twice the half's.  Every amplitude of the full
 state is available (`.amps` mirrors the half).
 
@@ -112,10 +112,9 @@ class SymmetricState(StateVector):
         return 2.0 * he.scalar("qaoa_expectation")
 
 
-# Fast runs with at least this many local qubits (three or more qubit sets,
-# so the low set is always a single-stage middle sweep) run in one
-# qaoa_run_layers call with the mirror fused into the low-set sweeps.
-FUSED_MIN_LOCAL = 22
+# Fast runs with at least this many local qubits (every symmetric run) go
+# through one qaoa_run_layers call with the mirror low set.
+FUSED_MIN_LOCAL = 12
 
 
 def _normalize_top_bit(eng: Engine) -> None:
@@ -133,8 +132,8 @@ def simulate_symmetric(g: Graph, params, exact: bool = False, fuse_expectation: 
                        state: SymmetricState | None = None, device: int = 0,
                        timing: bool = False, fused: bool | None = None) -> SymmetricState:
     """The p-level circuit on the x_{N-1} = 0 half of the state (see module doc).
-    ``fused``: None picks the one-call schedule whenever it applies (fast, N-1 >=
-    22); False forces the segmented run with separate mirror passes."""
+    ``fused``: None picks the one-call schedule whenever it applies (fast mode);
+    False forces the segmented run with one separate mirror pass per level."""
     from .circuit import level_arrays
 
     n = g.n
@@ -145,7 +144,7 @@ def simulate_symmetric(g: Graph, params, exact: bool = False, fuse_expectation: 
     if fused is None:
         fused = not exact and n - 1 >= FUSED_MIN_LOCAL
     if fused and (exact or n - 1 < FUSED_MIN_LOCAL):
-        raise ValueError("the fused symmetric schedule is fast-mode with N >= 23")
+        raise ValueError("the fused symmetric schedule is fast-mode only")
     he = state.half_engine if isinstance(state, SymmetricState) and state.n == n else None
     eng = he if he is not None else Engine(n - 1, device)
     eng.ensure_graph(g)

@@ -130,13 +130,15 @@ def test_symmetric_n34_p1_closed_form():
 
 
 @pytest.mark.parametrize("n,betas", [
-    (23, (0.4, 1.1, 2.0)),          # 22 local qubits: the smallest fused case
-    (25, (0.3, 2.9, 1.0, 2.7)),     # odd: u3r(24) + isolated node; second-form levels
-    (26, (2.95, 0.2, 3.05, 1.4, 0.6)),
+    (13, (0.4, 1.1, 2.0)),          # 12 local qubits: mirror low set + one 1-bit high set
+    (17, (0.9, 2.8)),               # two sets: the mirror low set is merged / first / last
+    (22, (0.3, 2.9, 1.0, 2.7)),     # second-form levels
+    (23, (2.95, 0.2, 3.05, 1.4, 0.6)),  # odd: u3r(22) + isolated node; three sets
+    (26, (0.7, 1.9, 2.6)),
 ])
 def test_fused_mirror_matches_segmented_and_oracle(oracle, n, betas):
-    """The low-set sweeps with the top qubit's RX fused (2-CTA clusters over
-    DSMEM, one qaoa_run_layers call) against the segmented run (one mirror pass
+    """The mirror low set (local qubits 0..10 plus the virtual top qubit in one
+    sweep, one qaoa_run_layers call) against the segmented run (one mirror pass
     per level) and the oracle's full state: amplitudes within 1e-12, <C> 1e-10."""
     from paper_2312_03019_b200.symmetric import simulate_symmetric
 
@@ -157,23 +159,20 @@ def test_fused_mirror_matches_segmented_and_oracle(oracle, n, betas):
 
 
 def test_fused_mirror_refusals():
-    """QAOA_RUN_MIRROR without QAOA_RUN_SHARDED: fast schedule, n_local >= 22,
-    a graph of n_local + 1 nodes; anything else is refused with a message."""
+    """QAOA_RUN_MIRROR without QAOA_RUN_SHARDED: fast schedule and a graph of
+    n_local + 1 nodes; anything else is refused with a message."""
     from paper_2312_03019_b200 import _lib
     from paper_2312_03019_b200.circuit import level_arrays
     from paper_2312_03019_b200.symmetric import simulate_symmetric
 
     pr = Q.params_from_seed(2, 0)
-    g = Q.random_regular_graph(22, 3, seed=1)
-    with pytest.raises(ValueError, match="fused"):
-        simulate_symmetric(g, pr, fused=True)  # 21 local qubits
     g24 = Q.random_regular_graph(24, 3, seed=1)
     with pytest.raises(ValueError, match="fused"):
         simulate_symmetric(g24, pr, exact=True, fused=True)
-    eng = Q.Engine(23)
+    eng = Q.Engine(22)
     try:
-        eng.ensure_graph(Q.random_regular_graph(22, 3, seed=1))  # n_local + 1 != nodes
-        tables, cs, ss = level_arrays(Q.random_regular_graph(22, 3, seed=1), pr)
+        eng.ensure_graph(g24)  # 24 nodes on 22 local qubits: not a half state
+        tables, cs, ss = level_arrays(g24, pr)
         with pytest.raises(ValueError, match="n_local \\+ 1"):
             eng.call("qaoa_run_layers", 2, _lib.dptr(np.ascontiguousarray(tables).view(np.float64)),
                      _lib.dptr(cs), _lib.dptr(ss), _lib.RUN_MIRROR)

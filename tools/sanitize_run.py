@@ -27,6 +27,14 @@ s = Q.init_uniform(22, max_qubits=22)
 s.engine().call("qaoa_set_layout_swap", 1)
 s = Q.simulate(g, Q.QaoaParams((0.3, 1.2), (0.5, 2.9)), "bitwise", max_qubits=22, state=s)
 Q.expectation(g, s)
+# symmetric half state: mirror low set (fused, merged at two sets and flow 1 at
+# three) and the segmented exact run with its mirror passes
+for n in (17, 24):
+    g = Q.random_regular_graph(n, 3, seed=n)
+    pr = Q.QaoaParams((0.3, 1.2, 2.2), (0.5, 2.9, 1.1))
+    for exact in (False, True):
+        s = Q.simulate(g, pr, "bitwise", exact=exact, symmetric=True, max_qubits=n)
+        Q.expectation(g, s)
 g = Q.random_regular_graph(16, 3, seed=1)
 shards = [CudaShard(14, r) for r in range(4)]
 simulate_sharded(g, Q.QaoaParams((0.3, 1.0), (2.9, 0.4)), shards, LocalExchanger(shards), 2)
