@@ -694,14 +694,24 @@ def run_ours(args, rank: int, world: int, local: int):
         for _ in range(max(args.warmup, 3) - 1):
             simulate_symmetric(g, params, state=ss)
         torch.cuda.synchronize(device)
+        sym_launch: list[float] = []
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            simulate_symmetric(g, params, state=ss)
+            simulate_symmetric(g, params, state=ss, timing=True)
             e_sym = Q.expectation(g, ss)
+            buf = (ctypes.c_float * 4096)()
+            k = L.qaoa_layer_timings(ss.half_engine.ptr, buf, 4096)
+            sym_launch.extend(buf[:k])
         sym_s = time.perf_counter() - t0
+        per_step = len(sym_launch) // max(args.steps, 1)
+        sym_dev_ms = sum(sym_launch) / max(args.steps, 1)
         sym = {"value": p * args.steps / sym_s, "unit": UNIT, "ms_per_step": 1e3 * sym_s / args.steps,
-               "timing": "wall clock over K host-driven steps (segmented run + one mirror pass "
-                         "per level), <C> read back every step",
+               "timing": "wall clock over K steps through simulate(..., symmetric=True) + "
+                         "expectation (one qaoa_run_layers call per step, <C> read back)",
+               "device_ms_per_step": sym_dev_ms,
+               "launch_ms_last_step": [round(x, 3) for x in sym_launch[-per_step:]],
+               "schedule": "fast; mirror low set (stored blocks u and ~u = virtual qubits 0..10 "
+                           f"and {n - 1} in one sweep), high sets on qubits 11..{n - 2}",
                "state": f"2^{n - 1} amplitudes (the x_{n - 1} = 0 half; psi(x) == psi(~x) bit for "
                         "bit), simulate(..., symmetric=True); not the headline",
                "expectation": e_sym, "expectation_rel_diff": abs(e_sym - expect_val) / abs(expect_val)}

@@ -347,13 +347,15 @@ GraphDev swap_graph(const GraphDev& g, int lo, int hi, int m) {
 // by the relabelling -- writes its tiles out of place with the bit ranges of set
 // 1 and the last set exchanged, so the set merged next always sits at bits
 // 12..: all merges run the set-1 geometry.  An even number of swaps per run
-// returns the state to identity order in its own buffer.
+// returns the state to identity order in its own buffer.  A symmetric run's
+// mirror low set (blocks u and ~u of 2048, qubits 11.. in the high sets) swaps
+// the same way: the complement commutes with the bit-range swap.
 void plan_swaps(qaoa_ctx* c, RunState& R) {
   R.swap = false;
   R.lay.assign(R.plan.size(), 0);
   R.do_swap.assign(R.plan.size(), 0);
   const int ns = (int)R.sets.size();
-  if (R.exact || R.weighted || R.sharded || R.mirror_fused || ns < 3 || c->swap_mode == 0) return;
+  if (R.exact || R.weighted || R.sharded || ns < 3 || c->swap_mode == 0) return;
   if (c->swap_mode < 0) {
     static int env = -2;
     if (env == -2) {

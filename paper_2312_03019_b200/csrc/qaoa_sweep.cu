@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   auto visit = [&](uint64_t b) -> uint64_t {
     if (C < 12 || !a.out) return b;
     const int k = a.sw_m / 2 < 4 ? a.sw_m / 2 : 4;
-    return swap_bit_ranges(b, k, a.sw_hi - 12, k);
+    return swap_bit_ranges(b, k, a.sw_hi - (MIR ? 11 : 12), k);  // tile number = index >> (MIR ? 11 : 12)
   };
   const uint64_t tile = visit((uint64_t)a.tile_lo + blockIdx.x);
   TileCtx tc;
@@ -199,8 +199,11 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
       acc = WGT ? expect_wacc<last>(v, &wcb[0], a.wc, tid, sk) : expect_acc<last>(v, &cb, tid, sk);
     if (MIR) {
       if (!(flags & kNoStore)) {
+        // out of place into the swapped layout: block u -> swap(u), and the
+        // complement commutes with the bit-range swap, so ~u -> ~swap(u)
+        const uint64_t u = a.out ? swap_bit_ranges(tile << 11, a.sw_lo, a.sw_hi, a.sw_m) >> 11 : tile;
         double2* ptr[kRegs];
-        mirror_ptrs<last>(amps, tile, 2ull * (uint64_t)a.ntiles, tid, ptr);
+        mirror_ptrs<last>(a.out ? a.out : amps, u, 2ull * (uint64_t)a.ntiles, tid, ptr);
 #pragma unroll
         for (int r = 0; r < kRegs; ++r) __stcs(ptr[r], v[r]);
       }
@@ -294,7 +297,7 @@ static cudaError_t launch_one(const SweepArgs& a, int grid, size_t smem, cudaStr
 // Mirror low set of a symmetric half state (kMirror, see sweep_kernel).
 template <bool WIDE>
 static cudaError_t launch_mirror(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {
-  if (a.carry != 12 || (a.flags & (kExact | kWeighted)) || a.out || a.ntiles < 1)
+  if (a.carry != 12 || (a.flags & (kExact | kWeighted)) || a.ntiles < 1)
     return cudaErrorInvalidValue;
   if (a.flags & kStage2) return launch_one<WIDE, 12, 2, false, true>(a, grid, smem, s);
   return launch_one<WIDE, 12, 1, false, true>(a, grid, smem, s);

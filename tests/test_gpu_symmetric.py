@@ -178,3 +178,23 @@ def test_fused_mirror_refusals():
                      _lib.dptr(cs), _lib.dptr(ss), _lib.RUN_MIRROR)
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("betas", [(0.4, 1.1, 2.0, 0.7), (2.9, 0.3, 2.2)])
+def test_fused_mirror_swapped_layout_bit_identical(betas):
+    """Mirror low-set sweeps written out of place into the swapped qubit layout
+    (high sets 11..15 and 16..20 of a 21-qubit half exchanged) equal the in-place
+    run bit for bit (N = 22)."""
+    from paper_2312_03019_b200.symmetric import simulate_symmetric
+
+    n = 22
+    g = Q.random_regular_graph(n, 3, seed=5)
+    pr = Q.QaoaParams(tuple(0.5 + 0.6 * k for k in range(len(betas))), betas)
+    runs = []
+    for mode in (0, 1):
+        s = simulate_symmetric(g, pr)
+        s.half_engine.call("qaoa_set_layout_swap", mode)
+        s = simulate_symmetric(g, pr, state=s)
+        runs.append((s.expectation(g), s.amps.copy()))
+    assert runs[0][0] == runs[1][0]
+    assert np.array_equal(runs[0][1], runs[1][1])

@@ -29,7 +29,7 @@ s = Q.simulate(g, Q.QaoaParams((0.3, 1.2), (0.5, 2.9)), "bitwise", max_qubits=22
 Q.expectation(g, s)
 # symmetric half state: mirror low set (fused, merged at two sets and flow 1 at
 # three) and the segmented exact run with its mirror passes
-for n in (17, 24):
+for n in (18, 24):
     g = Q.random_regular_graph(n, 3, seed=n)
     pr = Q.QaoaParams((0.3, 1.2, 2.2), (0.5, 2.9, 1.1))
     for exact in (False, True):
