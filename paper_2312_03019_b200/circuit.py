@@ -196,12 +196,13 @@ def simulate(
         raise ValueError(f"batch width must be 1, 2, 4, or 8, got {batch_width}")
     check_qubit_budget(g.n, max_qubits)
     if symmetric:
-        if backend == "baseline" or not launch_control or not store_state:
+        if backend == "baseline" or not launch_control:
             raise ValueError("symmetric=True runs the fused engine with launch control")
         from .symmetric import simulate_symmetric
 
         return simulate_symmetric(g, params, exact=exact, fuse_expectation=fuse_expectation,
-                                  state=state, device=device)
+                                  state=state, device=device,
+                                  store_state=store_state or exact)
     if backend == "baseline":
         return _simulate_gates(g, params, launch_control, threads, max_qubits, state)
     if state is not None and state.n == g.n:

@@ -749,6 +749,12 @@ int run_end(qaoa_ctx* c) {
                              : local_mask(c);
     c->g.cmask ^= all;
   }
+  // symmetric half state: a mask with the virtual top bit set describes the
+  // same data as its full complement (psi(v) == psi(~v)); keep the bit clear so
+  // reads see the stored half (without touching the fused <C>, which C(v) ==
+  // C(~v) leaves unchanged)
+  if (R.mirror_fused && ((c->g.cmask >> c->n) & 1ull))
+    c->g.cmask ^= (c->g.n_nodes >= 64 ? ~0ull : ((1ull << c->g.n_nodes) - 1ull));
   if (R.expect_fused) {
     if ((rc = reduce_to_host(c, R.grid, 0, &c->expect_value))) return rc;
     ++c->last_launches;

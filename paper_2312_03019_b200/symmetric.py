@@ -130,10 +130,13 @@ def _normalize_top_bit(eng: Engine) -> None:
 
 def simulate_symmetric(g: Graph, params, exact: bool = False, fuse_expectation: bool = True,
                        state: SymmetricState | None = None, device: int = 0,
-                       timing: bool = False, fused: bool | None = None) -> SymmetricState:
+                       timing: bool = False, fused: bool | None = None,
+                       store_state: bool = True) -> SymmetricState:
     """The p-level circuit on the x_{N-1} = 0 half of the state (see module doc).
     ``fused``: None picks the one-call schedule whenever it applies (fast mode);
-    False forces the segmented run with one separate mirror pass per level."""
+    False forces the segmented run with one separate mirror pass per level.
+    ``store_state=False`` (fused runs with the fused <C>): the last sweep only
+    reads; the state may then only give its expectation or be reused as state=."""
     from .circuit import level_arrays
 
     n = g.n
@@ -154,6 +157,8 @@ def simulate_symmetric(g: Graph, params, exact: bool = False, fuse_expectation: 
         # one call: the low-set sweeps apply the top qubit's RX themselves
         flags = _lib.RUN_MIRROR | (_lib.RUN_EXPECTATION if fuse_expectation else 0) | \
             (_lib.RUN_TIMING if timing else 0)
+        if not store_state and fuse_expectation:
+            flags |= _lib.RUN_EXPECT_ONLY
         eng.call("qaoa_run_layers", params.p, _lib.dptr(t.view(np.float64)), _lib.dptr(cs),
                  _lib.dptr(ss), flags)
         return _finish(eng, g, params, state, he)

@@ -58,3 +58,15 @@ def test_optimizer_errors():
     with pytest.raises(ValueError):
         Q.optimize(g, p=1, init_strategy="bogus")
     assert Q.approximation_ratio(Q.Graph.from_edges(3, []), 0.0) == 1.0
+
+
+def test_symmetric_evaluations_match_full_state():
+    """N >= 13 optimizer runs evaluate on the psi(x) == psi(~x) half state by
+    default; the Nelder-Mead history equals the full-state run's within 1e-10."""
+    g = Q.random_regular_graph(16, 3, seed=4)
+    a = Q.optimize(g, p=2, budget=60, seed=1, symmetric=True)
+    b = Q.optimize(g, p=2, budget=60, seed=1, symmetric=False)
+    assert a.evaluations == b.evaluations == 60
+    for (i, v), (j, w) in zip(a.history, b.history):
+        assert i == j and v == pytest.approx(w, rel=1e-10)
+    assert a.best_expectation == pytest.approx(b.best_expectation, rel=1e-10)

@@ -198,3 +198,18 @@ def test_fused_mirror_swapped_layout_bit_identical(betas):
         runs.append((s.expectation(g), s.amps.copy()))
     assert runs[0][0] == runs[1][0]
     assert np.array_equal(runs[0][1], runs[1][1])
+
+
+@pytest.mark.parametrize("betas", [(2.9,), (2.9, 0.4), (0.3, 2.8, 3.0), (0.5, 1.0)])
+def test_symmetric_expectation_only(betas):
+    """store_state=False (the optimizer's evaluations): the last sweep only reads;
+    <C> is right whatever the parity of second-form levels (which complement the
+    virtual top bit) and the state refuses reads."""
+    n = 20
+    g = Q.random_regular_graph(n, 3, seed=7)
+    pr = Q.QaoaParams(tuple(0.4 + 0.8 * k for k in range(len(betas))), betas)
+    e_full = Q.expectation(g, Q.simulate(g, pr, "bitwise", max_qubits=n))
+    s = Q.simulate(g, pr, "bitwise", symmetric=True, store_state=False, max_qubits=n)
+    assert Q.expectation(g, s) == pytest.approx(e_full, rel=1e-10)
+    with pytest.raises(Exception):
+        s.amps
