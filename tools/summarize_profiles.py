@@ -45,8 +45,8 @@ def launches(R):
     return agg, total
 
 
-def details(R):
-    rows = read_csv(os.path.join(ROOT, "gpurun_out", f"sweep_details_{R}.csv"))
+def details(R, prefix="sweep"):
+    rows = read_csv(os.path.join(ROOT, "gpurun_out", f"{prefix}_details_{R}.csv"))
     hdr = rows[0]
     ki, kn, mn, mv, mu = (hdr.index(x) for x in ("ID", "Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
     want = ["Duration", "DRAM Throughput", "Memory Throughput", "Registers Per Thread",
@@ -58,8 +58,8 @@ def details(R):
     return out
 
 
-def raw(R):
-    rows = read_csv(os.path.join(ROOT, "gpurun_out", f"sweep_raw_{R}.csv"))
+def raw(R, prefix="sweep"):
+    rows = read_csv(os.path.join(ROOT, "gpurun_out", f"{prefix}_raw_{R}.csv"))
     hdr = rows[0]
     units = dict(zip(hdr, rows[1]))
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
@@ -123,6 +123,25 @@ def main():
                          f"  bank conflicts: {r['bank_conflicts']:.3e}  warp instrs: {r['inst']:.3e}")
             lines.append("- top stalls: " + ", ".join(f"{k} {v}%" for k, v in r["stalls"]))
         lines.append("")
+    if os.path.exists(os.path.join(ROOT, "gpurun_out", f"sym_details_{R}.csv")):
+        # symmetric half state (tools/prof_sym.py 30 10): 2^29 amplitudes, 32 B each per sweep
+        lines += ["## `ncu --set full` of the symmetric half-state schedule (N=30 p=10, 2^29 "
+                  "stored amplitudes: launch-control, mirror low-set, merged sweeps)", ""]
+        sd, sr = details(R, "sym"), raw(R, "sym")
+        for (i, name), m in sd.items():
+            lines.append(f"### launch {i}: `{name}`")
+            for k, v in m.items():
+                lines.append(f"- {k}: {v}")
+            r = sr.get(i)
+            if r:
+                tb = (r["dram_read"] or 0) + (r["dram_write"] or 0)
+                lines.append(f"- DRAM read+write: {tb:.4e} B (algorithmic {32 * 2 ** (n - 1):.4e} B "
+                             "read+write, half that for the launch-control sweep)")
+                lines.append(f"- FP64 pipe active: {r['fp64_pipe_pct']}%  smem wavefronts: "
+                             f"{r['smem_wavefronts']:.3e}  bank conflicts: {r['bank_conflicts']:.3e}  "
+                             f"warp instrs: {r['inst']:.3e}")
+                lines.append("- top stalls: " + ", ".join(f"{k} {v}%" for k, v in r["stalls"]))
+            lines.append("")
     with open(os.path.join(ROOT, "profiles", f"{R}_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     full = [b for b in sweep_bytes if b > 0]
