@@ -230,7 +230,8 @@ QAOA_API int qaoa_read_cut_table(qaoa_ctx* ctx, uint64_t offset, uint64_t count,
 QAOA_API int qaoa_free_cut_table(qaoa_ctx* ctx);
 
 /* Per-launch device times (ms) of the last qaoa_run_layers run with
- * QAOA_RUN_TIMING; returns the number of launches (<= cap written). */
+ * QAOA_RUN_TIMING (or the one launch of the last qaoa_build_cut_table); returns
+ * the number of launches (<= cap written). */
 QAOA_API int qaoa_layer_timings(qaoa_ctx* ctx, float* ms, int cap);
 
 /* Number of kernels the last qaoa_run_layers call launched, and the HBM bytes

@@ -1619,9 +1619,16 @@ int qaoa_build_cut_table(qaoa_ctx* c) {
   }
   GraphDev gt = c->g;
   gt.cmask = 0;  // the table is of true indices, independent of the state
+  // the launch is bracketed by CUDA events (qaoa_layer_timings then returns its
+  // device time, without the host's launch latency)
+  if ((rc = record_event(c, true, 0))) return rc;
   if (c->n >= 11) CUDA_TRY(launch_cut_table_warps(c->cut_table, bytes_per, c->n, gt, c->stream));
   else CUDA_TRY(launch_cut_table(c->cut_table, bytes_per, c->n, gt, c->stream));
+  if ((rc = record_event(c, true, 1))) return rc;
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->events[0], c->events[1]));
+  c->times.assign(1, ms);
   return QAOA_OK;
 }
 
