@@ -201,8 +201,7 @@ def simulate(
         from .symmetric import simulate_symmetric
 
         return simulate_symmetric(g, params, exact=exact, fuse_expectation=fuse_expectation,
-                                  state=state, device=device,
-                                  store_state=store_state or exact)
+                                  state=state, device=device, store_state=store_state)
     if backend == "baseline":
         return _simulate_gates(g, params, launch_control, threads, max_qubits, state)
     if state is not None and state.n == g.n:

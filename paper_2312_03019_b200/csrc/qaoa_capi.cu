@@ -55,6 +55,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 struct SetDesc {
   int carry;
   int q;
+  bool mirror = false;  // symmetric half state: tile bit 11 is the virtual top qubit
 };
 
 struct SweepPlan {
@@ -200,14 +201,17 @@ int ensure_tables(qaoa_ctx* c, size_t n) {
   return QAOA_OK;
 }
 
-// mirror: a symmetric half state's fused schedule -- set 0 is the mirror low
-// set (local qubits 0..10 plus the virtual top qubit n, SetDesc{12, n}; see
-// sweep_kernel's MIR) and the high sets cover local qubits 11..n-1.
-std::vector<SetDesc> make_sets(int n, bool mirror = false) {
+// mirror: a symmetric half state's one-call schedule (sweep_kernel's MIR).
+// Fast: set 0 is the mirror low set (local qubits 0..10 plus the virtual top
+// qubit n, SetDesc{12, n}) and the high sets cover local qubits 11..n-1.
+// Exact: the high sets cover qubits 12..n including the virtual one, so the
+// top set carries it last (the reference applies qubit N-1 last).
+std::vector<SetDesc> make_sets(int n, bool mirror = false, bool exact = false) {
   std::vector<SetDesc> sets;
-  sets.push_back(SetDesc{12, mirror ? n : 0});
-  const int first = mirror ? 11 : 12;
-  const int rem = n - first;
+  const bool low_mirror = mirror && !exact;
+  sets.push_back(SetDesc{12, low_mirror ? n : 0, low_mirror});
+  const int first = low_mirror ? 11 : 12;
+  const int rem = n + (mirror && exact ? 1 : 0) - first;
   if (rem <= 0) return sets;
   const int chunks = (rem + 8) / 9;  // at most 9 mixed bits per high sweep (C >= 3)
   // the r = rem % chunks extra bits go to the middle chunks first, the ends
@@ -228,7 +232,7 @@ std::vector<SetDesc> make_sets(int n, bool mirror = false) {
   }
   int next = first;
   for (int ci = 0; ci < chunks; ++ci) {
-    sets.push_back(SetDesc{12 - size[ci], next});
+    sets.push_back(SetDesc{12 - size[ci], next, mirror && exact && ci == chunks - 1});
     next += size[ci];
   }
   return sets;
@@ -505,12 +509,11 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
   if (!R.from_state) c->g.cmask = 0;
 
   R.mirror_fused = (flags & QAOA_RUN_MIRROR) && !sharded;
-  if (R.mirror_fused && (R.exact || R.weighted || n_total != n + 1))
+  if (R.mirror_fused && (R.weighted || n_total != n + 1))
     return fail(QAOA_E_INVALID,
-                "QAOA_RUN_MIRROR without QAOA_RUN_SHARDED is the fused fast schedule: it needs a "
-                "graph of n_local + 1 nodes and no QAOA_RUN_EXACT (use the segmented run with "
-                "qaoa_mirror_rx otherwise)");
-  R.sets = make_sets(n, R.mirror_fused);
+                "QAOA_RUN_MIRROR without QAOA_RUN_SHARDED is the one-call symmetric schedule: it "
+                "needs an unweighted graph of n_local + 1 nodes");
+  R.sets = make_sets(n, R.mirror_fused, R.exact);
   R.plan = make_plan((int)R.sets.size(), p, R.exact, sharded, (flags & QAOA_RUN_MIRROR) != 0);
   // per-qubit RX factors of a level: the local qubits, plus the virtual top one
   // when its RX is fused into the low-set sweeps
@@ -684,7 +687,7 @@ int launch_plan_sweep(qaoa_ctx* c, int i, int64_t lo, int64_t cnt) {
     fl |= kStage1;
     a.rx1 = R.stages[sp.stage1];
   }
-  if (R.mirror_fused && sp.set == 0) fl |= kMirror;  // the mirror low set
+  if (R.mirror_fused && st.mirror) fl |= kMirror;  // a tile with the virtual top qubit
   if (sp.stage2 >= 0) {
     fl |= kStage2;
     a.rx2 = R.stages[sp.stage2];

@@ -42,26 +42,34 @@ namespace qb {
 // flight while the other computes (a persistent grid measured slower).
 // WGT: weighted cost (fast flows only; wbasis / apply_wcost in qaoa_tile.cuh).
 //
-// MIR (symmetric half state, fast flow 1): the "mirror low set".  The half
-// state of an N = n + 1 qubit state stores psi(v) for v_n = 0 (psi(v) ==
-// psi(~v)), so virtual index v lives at fold(v) = v_n ? ~v : v (n bits).  A
-// mirror tile u (u < 2^(n-12)) is the virtual tile with bits 0..10 and the
-// virtual top bit n: tile index t < 2048 is stored block u (2048 contiguous
-// amplitudes, ascending), t >= 2048 is block 2^(n-11) - 1 - u read backwards
-// (fold).  So one sweep mixes qubits 0..10 AND the virtual top qubit (tile bit
-// 11) with two contiguous 32 KB runs per tile and no cross-CTA traffic; the
-// cost geometry is the standard (C = 11, q = n) one in virtual coordinates
-// (C(v) = C(~v)).  The planner gives the high sets qubits 11..n-1.
-template <int M>
-__device__ __forceinline__ void mirror_ptrs(double2* amps, uint64_t u, uint64_t nblocks, int tid,
-                                            double2* (&ptr)[kRegs]) {
-  double2* const b1 = amps + (u << 11);                                  // t < 2048: b1 + t
-  double2* const b2 = amps + ((nblocks - 1ull - u) << 11) + 2047;        // t >= 2048: b2 - (t - 2048)
+// MIR (symmetric half state): a tile that contains the virtual top qubit.
+// The half state of an N = n + 1 qubit state stores psi(v) for v_n = 0
+// (psi(v) == psi(~v)), so virtual index v lives at fold(v) = v_n ? ~v : v (n
+// bits).  Tile bit 11 is the virtual bit n; tile bits 0..10 give the virtual
+// offset o(t) from the tile's virtual base, and fold puts the t >= 2048 half
+// at (2^n - 1) - o(t & 2047), i.e. the mirrored runs read backwards.  Two
+// geometries, both standard tiles in virtual coordinates (so the cut basis
+// and every butterfly are the ordinary ones):
+//  * fast schedule, the "mirror low set" (C = 12 flows, cut geometry (11, n)):
+//    qubits 0..10 and the virtual one; tile u is stored block u (2048
+//    amplitudes, ascending) plus block 2^(n-11) - 1 - u (backwards), two
+//    contiguous 32 KB runs; the high sets take qubits 11..n-1;
+//  * exact schedule, the folded top set (exact flow, geometry (C, q) with
+//    q + 11 - C = n): the top set's qubits then the virtual one, in the
+//    reference's increasing order (qubit N-1 last).
+// Only tiles whose top non-tile bit is 0 are visited (u < 2^(n-12)): the other
+// half are the same stored amplitudes.
+template <int C, int M>
+__device__ __forceinline__ void mirror_ptrs(double2* amps, uint64_t base, uint64_t Q, uint64_t mask_n,
+                                            int tid, int sk, double2* (&ptr)[kRegs]) {
   const int tp = tile_index<M>(tid, 0);
 #pragma unroll
-  for (int r = 0; r < kRegs; ++r) {
-    const int t = tp | tile_index<M>(0, r);  // disjoint bit parts
-    ptr[r] = (t & 2048) ? b2 - (t & 2047) : b1 + t;
+  for (int p = 0; p < kRegs; ++p) {
+    // skewed layout: physical register p holds logical p ^ sk
+    const int t = tp | (sk ? tile_index<M>(0, p ^ 1) : tile_index<M>(0, p));  // disjoint bit parts
+    const int lo = t & 2047;
+    const uint64_t o = base + (C >= 12 ? (uint64_t)lo : tile_off<C>(lo, Q));
+    ptr[p] = amps + ((t & 2048) ? mask_n - o : o);
   }
 }
 
@@ -94,7 +102,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   TileCtx tc;
   {
     const int low_bits = C >= 12 ? 0 : q - C;  // non-tile ranges [C, q) and [q + 12 - C, n)
-    tc.base = MIR ? (tile << 11)  // virtual index of tile element 0 (bits 0..10 and n clear)
+    tc.base = (MIR && C >= 12) ? (tile << 11)  // virtual index of tile element 0
                   : C >= 12 ? (tile << 12)
                   : (((tile & ((1ull << low_bits) - 1ull)) << C) | ((tile >> low_bits) << (q + 12 - C)));
   }
@@ -116,7 +124,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     const uint64_t pf_b = (uint64_t)a.tile_lo + blockIdx.x + a.pf_dist;
     if (a.pf_dist > 0 && pf_b < (uint64_t)(a.tile_lo + (a.tile_cnt ? a.tile_cnt : a.ntiles))) {
       const uint64_t pf_tile = visit(pf_b);
-      if (MIR) {
+      if (MIR && C < 12) {
+        // (exact folded top set: no prefetch)
+      } else if (MIR) {
         if (tid < 2) {
           const uint64_t blk = tid ? 2ull * (uint64_t)a.ntiles - 1ull - pf_tile : pf_tile;
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(amps + (blk << 11)), "r"(32768u)
@@ -138,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     }
     if (MIR) {
       double2* ptr[kRegs];
-      mirror_ptrs<2>(amps, tile, 2ull * (uint64_t)a.ntiles, tid, ptr);
+      mirror_ptrs<C, 2>(amps, tc.base, Q, ((uint64_t)a.ntiles << 12) - 1ull, tid, sk, ptr);
 #pragma unroll
       for (int r = 0; r < kRegs; ++r) v[r] = ld_tile(ptr[r]);
     } else {
@@ -153,7 +163,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         if (flags & kMidCost) wbasis<C>(a, tc.base, q, a.wu2, &wb[WGT ? 1 : 0]);
       }
       if (WGT && (flags & kExpect)) wcut_basis<C>(a, tc.base, q, &wcb[0]);
-      if (!WGT) cut_basis<WIDE, MIR ? 11 : C>(a, tc.base, q, &cb);  // MIR: q = n (virtual bit)
+      // the mirror low set's cut geometry is (11, n) (a.q = n)
+      if (!WGT) cut_basis<WIDE, (MIR && C >= 12) ? 11 : C>(a, tc.base, q, &cb);
     }
     // The basis is first read after the fast flow's first register exchange
     // (whose barrier then publishes it) unless a cost step precedes every
@@ -189,7 +200,16 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     }
     rx_regs2<A::g2, true>(v, r1a, r1b);
     if (flags & kExpect) acc = expect_acc<2>(v, &cb, tid, sk);
-    store_tile<C, 2>(amps, tc, Q, v, flags, sk);
+    if (MIR) {
+      if (!(flags & kNoStore)) {
+        double2* ptr[kRegs];
+        mirror_ptrs<C, 2>(amps, tc.base, Q, ((uint64_t)a.ntiles << 12) - 1ull, tid, sk, ptr);
+#pragma unroll
+        for (int r = 0; r < kRegs; ++r) __stcs(ptr[r], v[r]);
+      }
+    } else {
+      store_tile<C, 2>(amps, tc, Q, v, flags, sk);
+    }
   } else {
     fast_tile<C, FLOW, WGT>(v, a, &cb, wb, tid, sk, [&](auto from, auto to) {
       exchange<decltype(from)::value, decltype(to)::value>(buf, ts, v, sk);
@@ -201,9 +221,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
       if (!(flags & kNoStore)) {
         // out of place into the swapped layout: block u -> swap(u), and the
         // complement commutes with the bit-range swap, so ~u -> ~swap(u)
-        const uint64_t u = a.out ? swap_bit_ranges(tile << 11, a.sw_lo, a.sw_hi, a.sw_m) >> 11 : tile;
+        const uint64_t b = a.out ? swap_bit_ranges(tc.base, a.sw_lo, a.sw_hi, a.sw_m) : tc.base;
         double2* ptr[kRegs];
-        mirror_ptrs<last>(a.out ? a.out : amps, u, 2ull * (uint64_t)a.ntiles, tid, ptr);
+        mirror_ptrs<C, last>(a.out ? a.out : amps, b, Q, ((uint64_t)a.ntiles << 12) - 1ull, tid, sk, ptr);
 #pragma unroll
         for (int r = 0; r < kRegs; ++r) __stcs(ptr[r], v[r]);
       }
@@ -294,11 +314,27 @@ static cudaError_t launch_one(const SweepArgs& a, int grid, size_t smem, cudaStr
   return cudaGetLastError();
 }
 
-// Mirror low set of a symmetric half state (kMirror, see sweep_kernel).
+// Tiles with the virtual top qubit of a symmetric half state (kMirror, see
+// sweep_kernel): the fast mirror low set, or the exact folded top set.
 template <bool WIDE>
 static cudaError_t launch_mirror(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {
-  if (a.carry != 12 || (a.flags & (kExact | kWeighted)) || a.ntiles < 1)
-    return cudaErrorInvalidValue;
+  if ((a.flags & kWeighted) || a.ntiles < 1) return cudaErrorInvalidValue;
+  if (a.flags & kExact) {
+    if (a.out) return cudaErrorInvalidValue;
+    switch (a.carry) {
+      case 3: return launch_one<WIDE, 3, 0, false, true>(a, grid, smem, s);
+      case 4: return launch_one<WIDE, 4, 0, false, true>(a, grid, smem, s);
+      case 5: return launch_one<WIDE, 5, 0, false, true>(a, grid, smem, s);
+      case 6: return launch_one<WIDE, 6, 0, false, true>(a, grid, smem, s);
+      case 7: return launch_one<WIDE, 7, 0, false, true>(a, grid, smem, s);
+      case 8: return launch_one<WIDE, 8, 0, false, true>(a, grid, smem, s);
+      case 9: return launch_one<WIDE, 9, 0, false, true>(a, grid, smem, s);
+      case 10: return launch_one<WIDE, 10, 0, false, true>(a, grid, smem, s);
+      case 11: return launch_one<WIDE, 11, 0, false, true>(a, grid, smem, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  if (a.carry != 12) return cudaErrorInvalidValue;
   if (a.flags & kStage2) return launch_one<WIDE, 12, 2, false, true>(a, grid, smem, s);
   return launch_one<WIDE, 12, 1, false, true>(a, grid, smem, s);
 }

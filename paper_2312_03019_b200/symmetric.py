@@ -10,14 +10,17 @@ MaxCut QAOA keeps the state invariant under the global bit flip X^N:
 The engine therefore stores only the half with the top qubit N-1 = 0: a
 context of N-1 local qubits whose graph has N nodes (the top node is a fixed
 0 bit, like the shard bits of a sharded state).  RX on the top qubit pairs
-stored y with y ^ (2^(N-1) - 1).  Fast runs fold it into the low-set sweep
-(`qaoa_run_layers(..., QAOA_RUN_MIRROR)`): a "mirror tile" is stored block u
-of 2048 amplitudes plus block ~u read backwards, i.e. the virtual tile of
-qubits 0..10 and N-1, so one sweep mixes both and the high sets take qubits
-11..N-2; a level costs the sweeps of a full state of half the size.  Exact
-runs use one in-place pass (`qaoa_mirror_rx`) at the exchange points of a
-segmented run (`qaoa_run_begin(..., QAOA_RUN_SHARDED | QAOA_RUN_MIRROR)`),
-after the level's last set (the reference applies qubit N-1 last).  <C> and the
+stored y with y ^ (2^(N-1) - 1).  Every run is one `qaoa_run_layers(...,
+QAOA_RUN_MIRROR)` call whose tiles fold the virtual qubit in: virtual index v
+is stored at v or ~v, so a tile containing qubit N-1 is two sets of stored
+runs, the second read backwards.  The fast schedule uses the "mirror low set"
+(stored block u of 2048 amplitudes plus block ~u = the virtual tile of qubits
+0..10 and N-1; the high sets take 11..N-2); the exact schedule folds qubit N-1
+into the top set, after that set's qubits (the reference applies qubit N-1
+last).  A level costs the sweeps of a full state of half the size.  The older
+segmented form (one `qaoa_mirror_rx` pass per level at the exchange points of
+`qaoa_run_begin(..., QAOA_RUN_SHARDED | QAOA_RUN_MIRROR)`) stays available as
+``fused=False``.  <C> and the
 norm of the full state are twice the half's.  Every amplitude of the full
 state is available (`.amps` mirrors the half).
 
@@ -112,8 +115,8 @@ class SymmetricState(StateVector):
         return 2.0 * he.scalar("qaoa_expectation")
 
 
-# Fast runs with at least this many local qubits (every symmetric run) go
-# through one qaoa_run_layers call with the mirror low set.
+# Runs with at least this many local qubits (every symmetric run) go through
+# one qaoa_run_layers call.
 FUSED_MIN_LOCAL = 12
 
 
@@ -133,8 +136,8 @@ def simulate_symmetric(g: Graph, params, exact: bool = False, fuse_expectation: 
                        timing: bool = False, fused: bool | None = None,
                        store_state: bool = True) -> SymmetricState:
     """The p-level circuit on the x_{N-1} = 0 half of the state (see module doc).
-    ``fused``: None picks the one-call schedule whenever it applies (fast mode);
-    False forces the segmented run with one separate mirror pass per level.
+    ``fused``: None / True = the one-call schedule; False forces the segmented
+    run with one separate mirror pass per level.
     ``store_state=False`` (fused runs with the fused <C>): the last sweep only
     reads; the state may then only give its expectation or be reused as state=."""
     from .circuit import level_arrays
@@ -145,9 +148,7 @@ def simulate_symmetric(g: Graph, params, exact: bool = False, fuse_expectation: 
     if not g.is_unweighted:
         raise ValueError("the symmetric half-state mode runs unweighted graphs")
     if fused is None:
-        fused = not exact and n - 1 >= FUSED_MIN_LOCAL
-    if fused and (exact or n - 1 < FUSED_MIN_LOCAL):
-        raise ValueError("the fused symmetric schedule is fast-mode only")
+        fused = n - 1 >= FUSED_MIN_LOCAL
     he = state.half_engine if isinstance(state, SymmetricState) and state.n == n else None
     eng = he if he is not None else Engine(n - 1, device)
     eng.ensure_graph(g)
@@ -156,7 +157,7 @@ def simulate_symmetric(g: Graph, params, exact: bool = False, fuse_expectation: 
     if fused:
         # one call: the low-set sweeps apply the top qubit's RX themselves
         flags = _lib.RUN_MIRROR | (_lib.RUN_EXPECTATION if fuse_expectation else 0) | \
-            (_lib.RUN_TIMING if timing else 0)
+            (_lib.RUN_TIMING if timing else 0) | (_lib.RUN_EXACT if exact else 0)
         if not store_state and fuse_expectation:
             flags |= _lib.RUN_EXPECT_ONLY
         eng.call("qaoa_run_layers", params.p, _lib.dptr(t.view(np.float64)), _lib.dptr(cs),

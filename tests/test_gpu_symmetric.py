@@ -167,8 +167,6 @@ def test_fused_mirror_refusals():
 
     pr = Q.params_from_seed(2, 0)
     g24 = Q.random_regular_graph(24, 3, seed=1)
-    with pytest.raises(ValueError, match="fused"):
-        simulate_symmetric(g24, pr, exact=True, fused=True)
     eng = Q.Engine(22)
     try:
         eng.ensure_graph(g24)  # 24 nodes on 22 local qubits: not a half state
@@ -213,3 +211,21 @@ def test_symmetric_expectation_only(betas):
     assert Q.expectation(g, s) == pytest.approx(e_full, rel=1e-10)
     with pytest.raises(Exception):
         s.amps
+
+
+@pytest.mark.parametrize("n,betas", [(13, (0.4, 2.9)), (16, (1.1, 0.3, 2.2)), (21, (2.95, 0.6)),
+                                     (25, (0.8, 2.7, 1.3))])
+def test_exact_fold_matches_reference_order(oracle, n, betas):
+    """Exact schedule in one call: the virtual top qubit folded into the top
+    set (after that set's qubits) is bit for bit the reference -- and the
+    segmented run with its separate mirror passes."""
+    from paper_2312_03019_b200.symmetric import simulate_symmetric
+
+    g = Q.random_regular_graph(n, 3, seed=n + 1) if n % 2 == 0 else \
+        Q.Graph.from_edges(n, list(Q.random_regular_graph(n - 1, 3, seed=n).edges))
+    pr = Q.QaoaParams(tuple(0.7 + 0.5 * k for k in range(len(betas))), betas)
+    ref = oracle.simulate(n, g.row_mask, g.tot_edge, pr.gamma, pr.beta)
+    fo = simulate_symmetric(g, pr, exact=True)
+    seg = simulate_symmetric(g, pr, exact=True, fused=False)
+    assert np.array_equal(fo.amps, ref)
+    assert np.array_equal(seg.amps, ref)
