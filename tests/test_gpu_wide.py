@@ -251,7 +251,8 @@ def test_c3_n30_p10_vs_oracle_port(oracle):
     reference's arithmetic restated in C, pinned to the reference's own
     outputs) runs the whole circuit on the host's threads (~2 min); the GPU's
     exact schedule equals it bit for bit over all 2^30 amplitudes, the fast
-    schedule within 1e-12, <C> within 1e-10."""
+    schedule within 1e-12, <C> within 1e-10 -- and so do both schedules of the
+    symmetric half-state mode."""
     import os
 
     import psutil
@@ -281,3 +282,26 @@ def test_c3_n30_p10_vs_oracle_port(oracle):
             s.engine().close()
         assert worst <= AMP_TOL
         assert e == pytest.approx(eref, rel=EXP_RTOL)
+    # the symmetric half-state mode on the same config: the stored 2^29 half is
+    # the oracle's first half, and (psi(x) == psi(~x)) its reversal the second
+    # half -- bit for bit in the exact schedule, within 1e-12 in the fast one
+    from paper_2312_03019_b200.symmetric import simulate_symmetric
+
+    h = 1 << (n - 1)
+    for exact in (True, False):
+        s = simulate_symmetric(g, pr, exact=exact)
+        he = s.half_engine
+        try:
+            assert s.expectation(g) == pytest.approx(eref, rel=EXP_RTOL)
+            worst = 0.0
+            for off in range(0, h, chunk):
+                got = he.read(off, chunk)
+                lo = ref[off:off + chunk]
+                hi = ref[(1 << n) - off - chunk:(1 << n) - off][::-1]  # the mirrored indices
+                if exact:
+                    assert np.array_equal(got, lo) and np.array_equal(got, hi), off
+                else:
+                    worst = max(worst, float(np.max(np.abs(got - lo))), float(np.max(np.abs(got - hi))))
+        finally:
+            he.close()
+        assert worst <= AMP_TOL
