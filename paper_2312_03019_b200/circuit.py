@@ -277,7 +277,7 @@ def expectation(g: Graph, s: StateVector) -> float:
     fixed-order reduction; the fused value of the last simulate when valid."""
     if s.n != g.n:
         raise ValueError(f"state has {s.n} qubits but graph has {g.n} nodes")
-    if getattr(s, "half_engine", None) is not None and g.is_unweighted:
+    if getattr(s, "half_engine", None) is not None:
         return s.expectation(g)  # symmetric half state: twice the half's sum
     eng = s.engine()
     eng.ensure_graph(g)

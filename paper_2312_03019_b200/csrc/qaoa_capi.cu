@@ -509,10 +509,10 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
   if (!R.from_state) c->g.cmask = 0;
 
   R.mirror_fused = (flags & QAOA_RUN_MIRROR) && !sharded;
-  if (R.mirror_fused && (R.weighted || n_total != n + 1))
+  if (R.mirror_fused && n_total != n + 1)
     return fail(QAOA_E_INVALID,
                 "QAOA_RUN_MIRROR without QAOA_RUN_SHARDED is the one-call symmetric schedule: it "
-                "needs an unweighted graph of n_local + 1 nodes");
+                "needs a graph of n_local + 1 nodes");
   R.sets = make_sets(n, R.mirror_fused, R.exact);
   R.plan = make_plan((int)R.sets.size(), p, R.exact, sharded, (flags & QAOA_RUN_MIRROR) != 0);
   // per-qubit RX factors of a level: the local qubits, plus the virtual top one
@@ -593,8 +593,10 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
         if (sp.pre_cost == l || sp.mid_cost == l) set = sp.set;
       const SetDesc& sd = R.sets[set < 0 ? 0 : set];
       const std::complex<double> f = R.exact ? std::complex<double>(1.0, 0.0) : level_scale[l];
+      // the mirror low set's tile geometry is (11, n): node n is the virtual qubit
       CUDA_TRY(launch_wq_table(c->d_wq + (size_t)l * 4096, c->d_wedge, c->d_wu + (size_t)l * m, m,
-                               sd.carry, sd.q, make_double2(f.real(), f.imag()), c->stream));
+                               sd.mirror && sd.carry == 12 ? 11 : sd.carry, sd.q,
+                               make_double2(f.real(), f.imag()), c->stream));
     }
     CUDA_TRY(cudaStreamSynchronize(c->stream));  // hu is a host temporary
   }
@@ -627,7 +629,8 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
   if (R.expect_fused && R.weighted) {
     if (!c->d_wc) CUDA_TRY(cudaMalloc(&c->d_wc, 4096 * sizeof(double)));
     const SetDesc& sd = R.sets[R.plan.back().set];
-    CUDA_TRY(launch_wc_table(c->d_wc, c->d_wedge, c->d_w, c->n_wedges, sd.carry, sd.q, c->stream));
+    CUDA_TRY(launch_wc_table(c->d_wc, c->d_wedge, c->d_w, c->n_wedges,
+                             sd.mirror && sd.carry == 12 ? 11 : sd.carry, sd.q, c->stream));
   }
   R.no_store_last = (flags & QAOA_RUN_EXPECT_ONLY) && R.expect_fused;
   // the swapped layout only for runs the library drives end to end

@@ -158,11 +158,12 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   const bool need_cut = flags & (kPreCost | kMidCost | kExpect);
   if (need_cut) {
     if (tid < 32) {
+      constexpr int GC = (MIR && C >= 12) ? 11 : C;  // cut geometry (mirror low set: (11, n))
       if (WGT) {
-        if (flags & kPreCost) wbasis<C>(a, tc.base, q, a.wu1, &wb[0]);
-        if (flags & kMidCost) wbasis<C>(a, tc.base, q, a.wu2, &wb[WGT ? 1 : 0]);
+        if (flags & kPreCost) wbasis<GC>(a, tc.base, q, a.wu1, &wb[0]);
+        if (flags & kMidCost) wbasis<GC>(a, tc.base, q, a.wu2, &wb[WGT ? 1 : 0]);
       }
-      if (WGT && (flags & kExpect)) wcut_basis<C>(a, tc.base, q, &wcb[0]);
+      if (WGT && (flags & kExpect)) wcut_basis<GC>(a, tc.base, q, &wcb[0]);
       // the mirror low set's cut geometry is (11, n) (a.q = n)
       if (!WGT) cut_basis<WIDE, (MIR && C >= 12) ? 11 : C>(a, tc.base, q, &cb);
     }
@@ -318,7 +319,7 @@ static cudaError_t launch_one(const SweepArgs& a, int grid, size_t smem, cudaStr
 // sweep_kernel): the fast mirror low set, or the exact folded top set.
 template <bool WIDE>
 static cudaError_t launch_mirror(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {
-  if ((a.flags & kWeighted) || a.ntiles < 1) return cudaErrorInvalidValue;
+  if (a.ntiles < 1 || ((a.flags & kWeighted) && (a.flags & kExact))) return cudaErrorInvalidValue;
   if (a.flags & kExact) {
     if (a.out) return cudaErrorInvalidValue;
     switch (a.carry) {
@@ -335,6 +336,10 @@ static cudaError_t launch_mirror(const SweepArgs& a, int grid, size_t smem, cuda
     }
   }
   if (a.carry != 12) return cudaErrorInvalidValue;
+  if (a.flags & kWeighted) {
+    if (a.flags & kStage2) return launch_one<WIDE, 12, 2, true, true>(a, grid, smem, s);
+    return launch_one<WIDE, 12, 1, true, true>(a, grid, smem, s);
+  }
   if (a.flags & kStage2) return launch_one<WIDE, 12, 2, false, true>(a, grid, smem, s);
   return launch_one<WIDE, 12, 1, false, true>(a, grid, smem, s);
 }

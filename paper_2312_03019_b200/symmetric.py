@@ -25,8 +25,8 @@ norm of the full state are twice the half's.  Every amplitude of the full
 state is available (`.amps` mirrors the half).
 
 Half the HBM bytes and half the arithmetic per level; N=34 fits one B200.
-Opt-in (``simulate(..., symmetric=True)``); unweighted graphs with launch
-control.
+Opt-in (``simulate(..., symmetric=True)``), launch control; weighted graphs
+(the weighted cost is flip-symmetric too) in the fast schedule.
 """
 
 from __future__ import annotations
@@ -112,6 +112,9 @@ class SymmetricState(StateVector):
     def expectation(self, g: Graph) -> float:
         he = self.half_engine
         he.ensure_graph(g)
+        if not g.is_unweighted:  # float cut values, graph.py:144-151
+            he.ensure_weights(g)
+            return 2.0 * he.scalar("qaoa_expectation_weighted")
         return 2.0 * he.scalar("qaoa_expectation")
 
 
@@ -145,8 +148,9 @@ def simulate_symmetric(g: Graph, params, exact: bool = False, fuse_expectation: 
     n = g.n
     if n < 13:
         raise ValueError("the symmetric half-state mode needs at least 13 qubits")
-    if not g.is_unweighted:
-        raise ValueError("the symmetric half-state mode runs unweighted graphs")
+    if not g.is_unweighted and (exact or fused is False):
+        raise ValueError("the symmetric half-state mode runs weighted graphs in the fast "
+                         "one-call schedule only")
     if fused is None:
         fused = n - 1 >= FUSED_MIN_LOCAL
     he = state.half_engine if isinstance(state, SymmetricState) and state.n == n else None
@@ -160,8 +164,15 @@ def simulate_symmetric(g: Graph, params, exact: bool = False, fuse_expectation: 
             (_lib.RUN_TIMING if timing else 0) | (_lib.RUN_EXACT if exact else 0)
         if not store_state and fuse_expectation:
             flags |= _lib.RUN_EXPECT_ONLY
-        eng.call("qaoa_run_layers", params.p, _lib.dptr(t.view(np.float64)), _lib.dptr(cs),
-                 _lib.dptr(ss), flags)
+        if not g.is_unweighted:
+            # factored weighted cost (cost.py:147-159) on the same mirror tiles
+            eng.ensure_weights(g)
+            gm = np.ascontiguousarray(np.array(params.gamma, dtype=np.float64))
+            eng.call("qaoa_run_layers_weighted", params.p, _lib.dptr(gm), _lib.dptr(cs),
+                     _lib.dptr(ss), flags)
+        else:
+            eng.call("qaoa_run_layers", params.p, _lib.dptr(t.view(np.float64)), _lib.dptr(cs),
+                     _lib.dptr(ss), flags)
         return _finish(eng, g, params, state, he)
     flags = _lib.RUN_SHARDED | _lib.RUN_MIRROR | (_lib.RUN_EXACT if exact else 0) | \
         (_lib.RUN_EXPECTATION if fuse_expectation else 0) | (_lib.RUN_TIMING if timing else 0)

@@ -229,3 +229,25 @@ def test_exact_fold_matches_reference_order(oracle, n, betas):
     seg = simulate_symmetric(g, pr, exact=True, fused=False)
     assert np.array_equal(fo.amps, ref)
     assert np.array_equal(seg.amps, ref)
+
+
+@pytest.mark.parametrize("n,p", [(14, 2), (20, 3), (24, 2)])
+def test_weighted_symmetric_matches_full(n, p):
+    """Weighted graphs (compressed backend, factored weighted cost): the mirror
+    low set with the weighted cut basis against the full-state fast run
+    (amplitudes 1e-12, weighted <C> 1e-10), fused and read-back <C>."""
+    g = Q.random_regular_graph(n, 3, weighted=True, seed=n)
+    assert not g.is_unweighted
+    pr = Q.params_from_seed(p, n)
+    full = Q.simulate(g, pr, "compressed", max_qubits=n)
+    e_full = Q.expectation(g, full)
+    a_full = full.amps
+    sym = Q.simulate(g, pr, "compressed", symmetric=True, max_qubits=n)
+    assert isinstance(sym, Q.SymmetricState)
+    assert Q.expectation(g, sym) == pytest.approx(e_full, rel=1e-10)
+    assert np.max(np.abs(sym.amps - a_full)) <= 1e-12
+    # unfused <C> of a weighted half state (read-only reduction, doubled)
+    s2 = Q.simulate(g, pr, "compressed", symmetric=True, max_qubits=n, fuse_expectation=False)
+    assert Q.expectation(g, s2) == pytest.approx(e_full, rel=1e-10)
+    with pytest.raises(ValueError):
+        Q.simulate(g, pr, "compressed", symmetric=True, exact=True, max_qubits=n)
