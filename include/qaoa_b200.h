@@ -212,6 +212,11 @@ QAOA_API int qaoa_expectation_weighted(qaoa_ctx* ctx, double* out);
  * out_idx = first true index x in the block with base + cumsum(|a|^2)(x) > t
  * (numpy's searchsorted(cdf, u, 'right') on the unnormalised cdf). */
 QAOA_API int qaoa_block_norms(qaoa_ctx* ctx, int block_bits, double* out);
+/* The context holds the x_n = 0 half of an (n+1)-qubit flip-symmetric state
+ * (on = 1; QAOA_RUN_MIRROR runs): qaoa_block_norms / qaoa_sample_blocks then
+ * cover the 2^(n+1) virtual indices in true order (the upper half read from
+ * the complemented stored indices), the same sums and draws as the full state. */
+QAOA_API int qaoa_set_mirror(qaoa_ctx* ctx, int on);
 QAOA_API int qaoa_sample_blocks(qaoa_ctx* ctx, int block_bits, int64_t n_groups,
                                 const int64_t* group_block, const double* group_base,
                                 const int64_t* group_off, const double* targets, int64_t* out_idx);

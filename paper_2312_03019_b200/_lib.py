@@ -69,6 +69,7 @@ SIGNATURES = {
     "qaoa_run_layers": (_c_int, [_vp, _c_int, _dp, _dp, _dp, _c_int]),
     "qaoa_apply_rx_range": (_c_int, [_vp, _c_int, _c_int, _c_dbl, _c_dbl, _c_int]),
     "qaoa_set_layout_swap": (_c_int, [_vp, _c_int]),
+    "qaoa_set_mirror": (_c_int, [_vp, _c_int]),
     "qaoa_trim": (_c_int, [_vp]),
     "qaoa_get_cmask": (_c_int, [_vp, _u64p]),
     "qaoa_set_cmask": (_c_int, [_vp, _u64]),

@@ -296,8 +296,10 @@ def sample(s: StateVector, shots: int, seed: int = 0) -> np.ndarray:
         raise ValueError("shots must be at least 1")
     import ctypes
 
-    eng = s.engine()
-    bb = min(s.n, 12)
+    # a symmetric half state samples in place (its engine walks the virtual
+    # full index space, qaoa_set_mirror) instead of materialising the full state
+    eng = getattr(s, "half_engine", None) or s.engine()
+    bb = min(s.n - (1 if eng.n < s.n else 0), 12)
     norms = np.empty(1 << (s.n - bb), dtype=np.float64)
     eng.call("qaoa_block_norms", bb, _lib.dptr(norms))
     prefix = np.cumsum(norms)

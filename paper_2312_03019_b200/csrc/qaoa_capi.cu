@@ -153,6 +153,9 @@ struct qaoa_ctx {
   // second state buffer of the swapped qubit layout (allocated on first use)
   double2* amps2 = nullptr;
   int swap_mode = -1;  // qaoa_set_layout_swap: -1 policy, 0 off, 1 whenever applicable
+  // qaoa_set_mirror: the buffer is the x_n = 0 half of an (n+1)-qubit symmetric
+  // state; block norms and sampling then cover the 2^(n+1) virtual indices
+  bool mirror_view = false;
 };
 
 namespace {
@@ -972,6 +975,14 @@ int qaoa_trim(qaoa_ctx* c) {
   return QAOA_OK;
 }
 
+int qaoa_set_mirror(qaoa_ctx* c, int on) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (on && c->n >= 63) return fail(QAOA_E_INVALID, "a mirrored half state needs n_local < 63");
+  c->mirror_view = on != 0;
+  return QAOA_OK;
+}
+
 int qaoa_set_layout_swap(qaoa_ctx* c, int mode) {
   int rc = check_ctx(c);
   if (rc) return rc;
@@ -1517,10 +1528,12 @@ int qaoa_block_norms(qaoa_ctx* c, int block_bits, double* out) {
   if ((rc = require_stored(c))) return rc;
   if (block_bits < 0 || block_bits > 12 || block_bits > c->n || !out)
     return fail(QAOA_E_INVALID, "bad block size");
-  const uint64_t nb = 1ull << (c->n - block_bits);
+  const int bits = c->n + (c->mirror_view ? 1 : 0);
+  const uint64_t nb = 1ull << (bits - block_bits);
   double* d = nullptr;
   CUDA_TRY(cudaMalloc(&d, nb * sizeof(double)));
-  cudaError_t e = launch_block_norms(c->amps, block_bits, nb, c->g.cmask & local_mask(c), d, c->stream);
+  cudaError_t e = launch_block_norms(c->amps, block_bits, nb, c->g.cmask & local_mask(c),
+                                     c->mirror_view ? (1ull << c->n) : 0ull, d, c->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, nb * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   cudaFree(d);
@@ -1551,7 +1564,8 @@ int qaoa_sample_blocks(qaoa_ctx* c, int block_bits, int64_t n_groups, const int6
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_base, group_base, n_groups * sizeof(double), cudaMemcpyHostToDevice, c->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_off, group_off, (n_groups + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_t, targets, shots * sizeof(double), cudaMemcpyHostToDevice, c->stream);
-  if (e == cudaSuccess) e = launch_sample_blocks(c->amps, block_bits, c->g.cmask & local_mask(c), n_groups, d_gb,
+  if (e == cudaSuccess) e = launch_sample_blocks(c->amps, block_bits, c->g.cmask & local_mask(c),
+                                                 c->mirror_view ? (1ull << c->n) : 0ull, n_groups, d_gb,
                                                  d_base, d_off, d_t, d_out, c->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(out_idx, d_out, shots * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);

@@ -408,13 +408,22 @@ cudaError_t launch_expectation_weighted(const double2* amps, uint64_t n, uint64_
 // each hit block once in shared memory and binary-searches its targets.
 constexpr int kSampleBlockMax = 4096;
 
+// Stored position of true index x: x ^ lmask, and for a symmetric half state
+// (fold = 2^n, the virtual top bit) the upper half folded onto the stored one,
+// psi(v) = psi(~v): the sampling kernels then walk the 2^(n+1) virtual indices
+// in true order, the same sums as on the full state.
+__device__ __forceinline__ uint64_t stored_index(uint64_t x, uint64_t lmask, uint64_t fold) {
+  const uint64_t v = x ^ lmask;
+  return (v & fold) ? (~v & (fold - 1ull)) : v;
+}
+
 __global__ void block_norms_kernel(const double2* __restrict__ amps, int block_bits,
-                                   uint64_t lmask, double* __restrict__ out) {
+                                   uint64_t lmask, uint64_t fold, double* __restrict__ out) {
   __shared__ double scratch[kBlock / 32];
   const uint64_t base = (uint64_t)blockIdx.x << block_bits;
   double acc = 0.0;
   for (int i = threadIdx.x; i < (1 << block_bits); i += kBlock) {
-    const double2 a = amps[(base + i) ^ lmask];
+    const double2 a = amps[stored_index(base + i, lmask, fold)];
     acc += a.x * a.x + a.y * a.y;
   }
   const double t = block_sum<kBlock>(acc, scratch);
@@ -422,7 +431,7 @@ __global__ void block_norms_kernel(const double2* __restrict__ amps, int block_b
 }
 
 __global__ void sample_blocks_kernel(const double2* __restrict__ amps, int block_bits,
-                                     uint64_t lmask, const int64_t* __restrict__ gblock,
+                                     uint64_t lmask, uint64_t fold, const int64_t* __restrict__ gblock,
                                      const double* __restrict__ gbase,
                                      const int64_t* __restrict__ goff,
                                      const double* __restrict__ targets,
@@ -436,7 +445,7 @@ __global__ void sample_blocks_kernel(const double2* __restrict__ amps, int block
   const int lo = threadIdx.x * per;
   double run = 0.0;
   for (int i = lo; i < lo + per && i < len; ++i) {
-    const double2 a = amps[(base + i) ^ lmask];
+    const double2 a = amps[stored_index(base + i, lmask, fold)];
     run += a.x * a.x + a.y * a.y;
     cdf[i] = run;
   }
@@ -468,17 +477,17 @@ __global__ void sample_blocks_kernel(const double2* __restrict__ amps, int block
 }
 
 cudaError_t launch_block_norms(const double2* amps, int block_bits, uint64_t n_blocks,
-                               uint64_t lmask, double* out, cudaStream_t s) {
-  block_norms_kernel<<<(unsigned)n_blocks, kBlock, 0, s>>>(amps, block_bits, lmask, out);
+                               uint64_t lmask, uint64_t fold, double* out, cudaStream_t s) {
+  block_norms_kernel<<<(unsigned)n_blocks, kBlock, 0, s>>>(amps, block_bits, lmask, fold, out);
   return cudaGetLastError();
 }
 
-cudaError_t launch_sample_blocks(const double2* amps, int block_bits, uint64_t lmask,
+cudaError_t launch_sample_blocks(const double2* amps, int block_bits, uint64_t lmask, uint64_t fold,
                                  int64_t n_groups, const int64_t* gblock, const double* gbase,
                                  const int64_t* goff, const double* targets, int64_t* out,
                                  cudaStream_t s) {
-  sample_blocks_kernel<<<(unsigned)n_groups, kBlock, 0, s>>>(amps, block_bits, lmask, gblock, gbase,
-                                                              goff, targets, out);
+  sample_blocks_kernel<<<(unsigned)n_groups, kBlock, 0, s>>>(amps, block_bits, lmask, fold, gblock,
+                                                              gbase, goff, targets, out);
   return cudaGetLastError();
 }
 

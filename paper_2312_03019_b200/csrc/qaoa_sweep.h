@@ -124,8 +124,8 @@ cudaError_t launch_expectation_weighted(const double2* amps, uint64_t n, uint64_
                                         const int* ei, const int* ej, const double* w, int m,
                                         double* partials, int grid, cudaStream_t s);
 cudaError_t launch_block_norms(const double2* amps, int block_bits, uint64_t n_blocks,
-                               uint64_t lmask, double* out, cudaStream_t s);
-cudaError_t launch_sample_blocks(const double2* amps, int block_bits, uint64_t lmask,
+                               uint64_t lmask, uint64_t fold, double* out, cudaStream_t s);
+cudaError_t launch_sample_blocks(const double2* amps, int block_bits, uint64_t lmask, uint64_t fold,
                                  int64_t n_groups, const int64_t* gblock, const double* gbase,
                                  const int64_t* goff, const double* targets, int64_t* out,
                                  cudaStream_t s);

@@ -47,6 +47,7 @@ class SymmetricState(StateVector):
 
     def __init__(self, n: int, engine: Engine):
         StateVector.__init__(self, n, engine=engine)
+        engine.call("qaoa_set_mirror", 1)  # sampling walks the 2^n virtual indices
 
     @property
     def half_engine(self) -> Engine | None:

@@ -251,3 +251,20 @@ def test_weighted_symmetric_matches_full(n, p):
     assert Q.expectation(g, s2) == pytest.approx(e_full, rel=1e-10)
     with pytest.raises(ValueError):
         Q.simulate(g, pr, "compressed", symmetric=True, exact=True, max_qubits=n)
+
+
+def test_symmetric_sampling_in_place():
+    """Sampling a symmetric half state walks the virtual full index space on the
+    device (qaoa_set_mirror): the same draws as sampling the full state, and no
+    full-size copy is made."""
+    n = 20
+    g = Q.random_regular_graph(n, 3, seed=9)
+    pr = Q.params_from_seed(3, 2)
+    full = Q.simulate(g, pr, "bitwise", exact=True, max_qubits=n)
+    sym = Q.simulate(g, pr, "bitwise", exact=True, symmetric=True, max_qubits=n)
+    a = Q.sample(full, 4000, seed=5)
+    b = Q.sample(sym, 4000, seed=5)
+    assert sym.half_engine is not None  # still the half: nothing materialised
+    assert np.array_equal(a, b)
+    assert b.min() >= 0 and b.max() < (1 << n)
+    assert (b >= (1 << (n - 1))).any()  # draws from the mirrored half too
