@@ -224,6 +224,11 @@ __device__ __forceinline__ int pack_basis(int d, int adjl) {
 
 template <bool WIDE, int C>
 __device__ __forceinline__ void cut_basis(const SweepArgs& a, uint64_t base, int q, CutBasis* cb) {
+#if defined(QB_SKIP) && (QB_SKIP & 64)
+  // probe builds only: a zero basis (every C(x) = 0) instead of the per-tile work
+  if ((threadIdx.x & 31) < 14) reinterpret_cast<int*>(cb)[threadIdx.x & 31] = 0;
+  return;
+#endif
   const uint64_t tile_phys = (C >= 12) ? 0xFFFull
                                        : (((1ull << C) - 1ull) | (((1ull << (12 - C)) - 1ull) << q));
   const uint64_t h = (a.g.x_hi ^ a.g.cmask ^ base) & ~tile_phys;
@@ -630,7 +635,8 @@ using ic = std::integral_constant<int, V>;
 // Timing-decomposition switches for tools/sweep_probe builds only (the library
 // is built with QB_SKIP = 0): bit 0 skips the shared-memory exchanges, bit 1
 // the lane transposes, bit 2 the cost phase, bit 3 the RX butterflies; inside
-// the cost (apply_cost) bit 4 the table gather, bit 5 the cut counts.
+// the cost (apply_cost) bit 4 the table gather, bit 5 the cut counts; bit 6
+// replaces the per-tile cut basis (cut_basis) by a zero basis.
 constexpr bool kDoX = !(QB_SKIP & 1), kDoT = !(QB_SKIP & 2), kDoC = !(QB_SKIP & 4),
                kDoR = !(QB_SKIP & 8);
 
