@@ -269,7 +269,7 @@ def run_reference(args, rank: int, world: int):
     line = {
         "impl": "reference", "metric": METRIC, "value": layers, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": workload_name(args),
                    "n_qubits": n, "p": p, "graph": args.graph,
@@ -737,7 +737,9 @@ def run_ours(args, rank: int, world: int, local: int):
             "metric": METRIC, "value": layers_per_s, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            # N=1 is the base point of the --gpus N curve (default: strong, the
+            # same N-qubit state sharded over more GPUs)
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "c128", "data": "synthetic",
             "config": {"workload": workload_name(args),
                        "n_qubits": n, "p": p, "graph": args.graph,
                        "schedule": "exact" if args.exact else "fast",
