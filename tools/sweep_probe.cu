@@ -175,7 +175,85 @@ __global__ void fill_random(double2* a, uint64_t n) {
   }
 }
 
+// Concurrency probe: sweep_probe conc N REPS: the low-set sweep S0 on the tiles
+// of one half of the state and the merged set-1 sweep on the other half
+// (disjoint amplitudes: S0 tiles [0, T/2) have bit N-1 = 0, merged tiles
+// [T/2, T) have bit N-1 = 1), once back to back on one stream and once
+// concurrently on two streams.
+static int conc_mode(int n, int reps) {
+  const uint64_t size = 1ull << n;
+  double2* amps;
+  if (cudaMalloc(&amps, 16 * size) != cudaSuccess) return 1;
+  fill_random<<<4096, 256>>>(amps, size);
+  GraphDev g;
+  memset(&g, 0, sizeof(g));
+  g.n_nodes = n;
+  int E = 0;
+  auto add = [&](int i, int j) {
+    if (i > j) { int t = i; i = j; j = t; }
+    if ((g.rm[i] >> j) & 1) return;
+    g.rm[i] |= 1ull << j; g.adj[i] |= 1ull << j; g.adj[j] |= 1ull << i; ++E;
+  };
+  for (int i = 0; i < n; ++i) add(i, (i + 1) % n);
+  for (int i = 0; i < n / 2; ++i) add(i, i + n / 2);
+  g.tot_edge = E;
+  double2* tab;
+  cudaMalloc(&tab, sizeof(double2) * (E + 1) * 2);
+  double2* h = (double2*)malloc(sizeof(double2) * (E + 1) * 2);
+  for (int k = 0; k < 2 * (E + 1); ++k) h[k] = make_double2(cos(0.1 * k), sin(0.1 * k));
+  cudaMemcpy(tab, h, sizeof(double2) * (E + 1) * 2, cudaMemcpyHostToDevice);
+  const int64_t T = (int64_t)(size >> 12);
+  const int m = (n - 12 + 1) / 2;
+  SweepArgs s0, mg;
+  memset(&s0, 0, sizeof(s0));
+  s0.amps = amps; s0.table = tab; s0.table2 = tab + (E + 1); s0.g = g; s0.ntiles = T;
+  s0.carry = 12; s0.q = 0; s0.rx1 = RxStage{0.3, 0.0, 1}; s0.table_len = E + 1; s0.flags = kStage1;
+  mg = s0;
+  mg.carry = 12 - m; mg.q = 12; mg.rx2 = RxStage{-0.2, 0.0, 1}; mg.flags = kStage1 | kMidCost | kStage2;
+  const int K = getenv("CONC_CHUNKS") ? atoi(getenv("CONC_CHUNKS")) : 1;
+  cudaStream_t sa, sb;
+  cudaStreamCreateWithFlags(&sa, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking);
+  cudaEvent_t e0, e1, ea, eb;
+  cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&ea); cudaEventCreate(&eb);
+  auto half = [&](SweepArgs a, int64_t lo, cudaStream_t st) {
+    for (int k = 0; k < K; ++k) {
+      a.tile_lo = lo + k * (T / 2 / K);
+      a.tile_cnt = T / 2 / K;
+      launch_sweep(a, (int)a.tile_cnt, st);
+    }
+  };
+  float t_seq = 0, t_conc = 0, t_s0 = 0, t_mg = 0;
+  for (int mode = 0; mode < 4; ++mode) {
+    for (int it = 0; it < 2; ++it) {  // warm-up pass, then timed
+      cudaDeviceSynchronize();
+      cudaEventRecord(e0, sa);
+      for (int r = 0; r < reps; ++r) {
+        if (mode == 0) { half(s0, 0, sa); half(mg, T / 2, sa); }
+        else if (mode == 1) {
+          cudaEventRecord(ea, sa);
+          cudaStreamWaitEvent(sb, ea, 0);
+          half(s0, 0, sa); half(mg, T / 2, sb);
+          cudaEventRecord(eb, sb);
+          cudaStreamWaitEvent(sa, eb, 0);
+        } else if (mode == 2) { half(s0, 0, sa); }
+        else { half(mg, T / 2, sa); }
+      }
+      cudaEventRecord(e1, sa);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ms /= reps;
+      if (it) (mode == 0 ? t_seq : mode == 1 ? t_conc : mode == 2 ? t_s0 : t_mg) = ms;
+    }
+  }
+  printf("n=%d chunks=%d: S0 half %.3f ms, merged half %.3f ms, back to back %.3f ms, concurrent %.3f ms (%.3f of back to back) %s\n",
+         n, K, t_s0, t_mg, t_seq, t_conc, t_conc / t_seq, cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && strcmp(argv[1], "conc") == 0) return conc_mode(atoi(argv[2]), atoi(argv[3]));
   if (argc > 1 && strcmp(argv[1], "cut") == 0)
     return cut_mode(atoi(argv[2]), atoi(argv[3]), argc > 4 ? atoi(argv[4]) : 0);
   if (argc > 1 && strcmp(argv[1], "check") == 0)
