@@ -143,6 +143,11 @@ struct qaoa_ctx {
   double2* d_wq = nullptr;
   size_t d_wq_cap = 0;
   double* d_wc = nullptr;  // tile-internal cut weights of the last sweep's set (fused weighted <C>)
+  // launch control on the TMA-fed kernel: per-tile cut bases and gen x phase table
+  void* d_basis = nullptr;
+  size_t d_basis_cap = 0;
+  double2* d_gen_tab = nullptr;
+  int d_gen_tab_cap = 0;
   // timing
   std::vector<cudaEvent_t> events;
   std::vector<float> times;
@@ -647,6 +652,16 @@ int run_begin(qaoa_ctx* c, int p, const double* phase_tables, const double* cs, 
   return QAOA_OK;
 }
 
+// QAOA_GEN_AUX=0 disables launch_gen_aux (A/B; default on).
+bool gen_aux_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("QAOA_GEN_AUX");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 // Launch plan sweep i on tiles [lo, lo + cnt) (cnt = 0: all tiles).
 int launch_plan_sweep(qaoa_ctx* c, int i, int64_t lo, int64_t cnt) {
   RunState& R = c->run;
@@ -724,6 +739,29 @@ int launch_plan_sweep(qaoa_ctx* c, int i, int64_t lo, int64_t cnt) {
   if (last && R.expect_fused) fl |= kExpect;
   if (last && R.no_store_last) fl |= kNoStore;
   a.flags = fl;
+  if ((fl & kGen) && (fl & kPreCost) && sweep_uses_tma(a) && gen_aux_enabled()) {
+    // launch control on the TMA-fed kernel: tile bases built ahead (off the
+    // per-tile critical path) and the uniform amplitude folded into the table
+    const size_t need = (size_t)kBasisEntryBytes * (size_t)a.ntiles;
+    if (c->d_basis_cap < need) {
+      if (c->d_basis) cudaFree(c->d_basis);
+      c->d_basis = nullptr;
+      c->d_basis_cap = 0;
+      CUDA_TRY(cudaMalloc(&c->d_basis, need));
+      c->d_basis_cap = need;
+    }
+    if (c->d_gen_tab_cap < te) {
+      if (c->d_gen_tab) cudaFree(c->d_gen_tab);
+      c->d_gen_tab = nullptr;
+      c->d_gen_tab_cap = 0;
+      CUDA_TRY(cudaMalloc(&c->d_gen_tab, sizeof(double2) * (size_t)te));
+      c->d_gen_tab_cap = te;
+    }
+    CUDA_TRY(launch_gen_aux(a, c->d_basis, c->d_gen_tab, c->stream));
+    a.basis_tab = c->d_basis;
+    a.table = c->d_gen_tab;
+    a.flags = fl | kGenTab;
+  }
   CUDA_TRY(launch_sweep(a, R.grid, c->stream));
   ++c->last_launches;
   const double frac = cnt ? (double)cnt / (double)a.ntiles : 1.0;
@@ -828,6 +866,8 @@ void qaoa_destroy(qaoa_ctx* c) {
   if (c->d_wq) cudaFree(c->d_wq);
   if (c->d_wc) cudaFree(c->d_wc);
   if (c->amps2) cudaFree(c->amps2);
+  if (c->d_basis) cudaFree(c->d_basis);
+  if (c->d_gen_tab) cudaFree(c->d_gen_tab);
   for (auto e : c->events) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -971,6 +1011,11 @@ int qaoa_trim(qaoa_ctx* c) {
   if (c->cut_table) {
     cudaFree(c->cut_table);
     c->cut_table = nullptr;
+  }
+  if (c->d_basis) {
+    cudaFree(c->d_basis);
+    c->d_basis = nullptr;
+    c->d_basis_cap = 0;
   }
   return QAOA_OK;
 }

@@ -297,6 +297,56 @@ cudaError_t launch_wc_table(double* c_out, const int2* wedge, const double* w, i
   return cudaGetLastError();
 }
 
+// ---- launch-control helpers (launch_gen_aux) ----------------------------------
+// One warp per tile: the same cut basis the sweep's warp 0 would build.
+template <bool WIDE, int C>
+__global__ void basis_table_kernel(const __grid_constant__ SweepArgs a, CutBasis* out, int64_t cnt) {
+  const int64_t w = (int64_t)((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
+  if (w >= cnt) return;  // warp-uniform
+  const uint64_t tile = (uint64_t)a.tile_lo + (uint64_t)w;
+  cut_basis<WIDE, C>(a, tile_base<C>(tile, a.q), a.q, out + tile);
+}
+
+__global__ void gen_table_kernel(double2* __restrict__ out, const double2* __restrict__ in, double2 gen,
+                                 int len) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < len) out[k] = cmul_np(gen, in[k]);
+}
+
+template <bool WIDE, int C>
+static void launch_basis_c(const SweepArgs& a, CutBasis* out, int64_t cnt, cudaStream_t s) {
+  const int64_t threads = cnt * 32;
+  basis_table_kernel<WIDE, C><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a, out, cnt);
+}
+
+template <bool WIDE>
+static cudaError_t launch_basis_w(const SweepArgs& a, CutBasis* out, int64_t cnt, cudaStream_t s) {
+  switch (a.carry) {
+    case 3: launch_basis_c<WIDE, 3>(a, out, cnt, s); break;
+    case 4: launch_basis_c<WIDE, 4>(a, out, cnt, s); break;
+    case 5: launch_basis_c<WIDE, 5>(a, out, cnt, s); break;
+    case 6: launch_basis_c<WIDE, 6>(a, out, cnt, s); break;
+    case 7: launch_basis_c<WIDE, 7>(a, out, cnt, s); break;
+    case 8: launch_basis_c<WIDE, 8>(a, out, cnt, s); break;
+    case 9: launch_basis_c<WIDE, 9>(a, out, cnt, s); break;
+    case 10: launch_basis_c<WIDE, 10>(a, out, cnt, s); break;
+    case 12: launch_basis_c<WIDE, 12>(a, out, cnt, s); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gen_aux(const SweepArgs& a, void* basis_out, double2* gen_table, cudaStream_t s) {
+  static_assert(sizeof(CutBasis) == kBasisEntryBytes, "basis entry = 16 ints (the TMA kernel's stride)");
+  if (!(a.flags & kGen) || !(a.flags & kPreCost) || !a.table || a.table_len < 1) return cudaErrorInvalidValue;
+  const int64_t cnt = a.tile_cnt ? a.tile_cnt : a.ntiles;
+  CutBasis* out = reinterpret_cast<CutBasis*>(basis_out);
+  cudaError_t e = a.g.n_nodes > 32 ? launch_basis_w<true>(a, out, cnt, s) : launch_basis_w<false>(a, out, cnt, s);
+  if (e != cudaSuccess) return e;
+  gen_table_kernel<<<(a.table_len + 127) / 128, 128, 0, s>>>(gen_table, a.table, a.gen, a.table_len);
+  return cudaGetLastError();
+}
+
 size_t sweep_smem_bytes(int) { return (size_t)kSlots * sizeof(double2); }
 
 template <bool WIDE, int C, int FLOW, bool WGT = false, bool MIR = false>

@@ -21,6 +21,7 @@ enum SweepFlags : uint32_t {
   kWeighted = 1u << 9, // weighted cost: factored per-edge phases (see apply_wcost)
   kMirror = 1u << 10,  // symmetric half state: RX on the virtual top qubit after the
                        // stage (pairs tile T with tile ~T, a 2-CTA cluster; see qaoa_sweep.cu)
+  kGenTab = 1u << 11,  // launch control with `table` = gen x phase table (cost = gather only)
 };
 
 struct SweepArgs {
@@ -60,7 +61,17 @@ struct SweepArgs {
   // swapped (the swapped qubit layout of qaoa_capi.cu); nullptr = in place
   double2* out;
   int sw_lo, sw_hi, sw_m;
+  // launch-control sweeps on the TMA-fed kernel: per-tile cut bases built ahead
+  // by launch_gen_aux (64 B per tile, indexed by absolute tile); nullptr = warp 0
+  // builds each tile's basis in the sweep
+  const void* basis_tab;
 };
+// Launch-control helpers (fast schedule, TMA-fed kernel): the cut basis of every
+// tile of [a.tile_lo, a.tile_lo + cnt) into basis_out (kBasisEntryBytes per
+// tile) and gen_table[k] = cmul_np(a.gen, a.table[k]) for k < a.table_len (the
+// product the sweep would form per amplitude: bit-identical).
+constexpr int kBasisEntryBytes = 64;
+cudaError_t launch_gen_aux(const SweepArgs& a, void* basis_out, double2* gen_table, cudaStream_t s);
 // Tile-internal phase table of one weighted cost level for tile geometry (C, q):
 // Q[t] = scale * prod over edges with both endpoints tile nodes of u_e (equal
 // true bits) or conj(u_e) (different), t = true tile index.

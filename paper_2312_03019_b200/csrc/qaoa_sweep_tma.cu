@@ -205,6 +205,15 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
 
   unsigned long long* ctr = ta.counter;
   bool last = false;
+  // launch control with a prebuilt basis table: lanes 0..15 of warp 0 hold the
+  // next tile's 64-byte entry (loaded one tile ahead in the static order)
+  const int* btab = reinterpret_cast<const int*>(a.basis_tab);
+  const bool gen_prefetch = gen && btab && !(DYN && !ta.gen_static);
+  int bnext = 0;
+  if (gen_prefetch && tid < 16) {
+    const uint64_t t0 = blockIdx.x + (uint64_t)grp * stride;
+    if (t0 < ntiles) bnext = __ldcg(btab + (lo + t0) * 16 + tid);
+  }
   for (uint32_t j = 0;; ++j) {
     if (last) break;
     uint64_t tile;
@@ -221,7 +230,17 @@ __global__ void __launch_bounds__(kCtaThreads, 1) sweep_tma_kernel(const __grid_
         tile = blockIdx.x + (uint64_t)(2 * j + grp) * stride;
       }
       if (tile >= ntiles) break;
-      if (need_cut && tid < 32) cut_basis<WIDE, C>(a, tile_base<C>(lo + tile, q), q, cb);
+      if (need_cut && btab) {
+        // the prebuilt basis (launch_gen_aux): a 56-byte copy instead of the
+        // per-tile popcount reduction on the group's critical path
+        if (tid < 14) reinterpret_cast<int*>(cb)[tid] = gen_prefetch ? bnext : __ldcg(btab + (lo + tile) * 16 + tid);
+        if (gen_prefetch && tid < 16) {
+          const uint64_t nt = blockIdx.x + (uint64_t)(2 * (j + 1) + grp) * stride;
+          if (nt < ntiles) bnext = __ldcg(btab + (lo + nt) * 16 + tid);
+        }
+      } else if (need_cut && tid < 32) {
+        cut_basis<WIDE, C>(a, tile_base<C>(lo + tile, q), q, cb);
+      }
 #pragma unroll
       for (int r = 0; r < kRegs; ++r) v[r] = a.gen;
       group_bar(bar_id);  // cut basis published; WAR on the exchange buffer / next_tile
@@ -444,7 +463,14 @@ int sweep_impl(const SweepArgs& a) {
   if ((a.flags & (kExact | kWeighted | kMirror)) || a.carry == 11 || a.ntiles < 1 || a.out) return 0;
   const int env = impl_env();
   if (env != 3) return env;
-  if (a.flags & kGen) return 2;
+  if (a.flags & kGen) {  // QAOA_GEN_IMPL overrides for launch control only (A/B)
+    static int gi = -2;
+    if (gi == -2) {
+      const char* e = getenv("QAOA_GEN_IMPL");
+      gi = e ? atoi(e) : -1;
+    }
+    return gi >= 0 ? gi : 2;
+  }
   const bool wide_span = a.carry < 12 && a.q + 12 - a.carry + 4 > 28;
   if ((a.flags & kStage2) && wide_span && a.carry == 3) return 2;
   return 0;

@@ -554,6 +554,18 @@ __device__ __forceinline__ void apply_cost(double2 (&v)[kRegs], const CutBasis* 
   }
 }
 
+// Launch control with the pre-multiplied table (kGenTab): every register
+// starts as gen, so gen x phase is a table entry (same rounding as apply_cost).
+template <int M>
+__device__ __forceinline__ void apply_gen_phase(double2 (&v)[kRegs], const CutBasis* cb,
+                                                const double2* __restrict__ gtab, int e,
+                                                int tid = threadIdx.x, int sk = 0) {
+  int c[16];
+  cut16<M>(cb, c, tid, sk);
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) v[r] = ld_phase(gtab + (e - c[r]));
+}
+
 template <int M>
 __device__ __forceinline__ double expect_acc(const double2 (&v)[kRegs], const CutBasis* cb,
                                              int tid = threadIdx.x, int sk = 0) {
@@ -654,6 +666,7 @@ __device__ __forceinline__ void fast_tile(double2 (&v)[kRegs], const SweepArgs& 
   const double r1a = a.rx1.a, r2a = a.rx2.a;
   if (a.flags & kPreCost) {
     if (WGT) apply_wcost<2>(v, &wb[0], a.wq1, tid, sk);
+    else if (kDoC && (a.flags & kGenTab)) apply_gen_phase<2>(v, cb, a.table, e, tid, sk);
     else if (kDoC) apply_cost<2>(v, cb, a.table, e, tid, sk);
   }
   if (C >= 12) {
