@@ -742,25 +742,29 @@ int launch_plan_sweep(qaoa_ctx* c, int i, int64_t lo, int64_t cnt) {
   if ((fl & kGen) && (fl & kPreCost) && sweep_uses_tma(a) && gen_aux_enabled()) {
     // launch control on the TMA-fed kernel: tile bases built ahead (off the
     // per-tile critical path) and the uniform amplitude folded into the table
+    // (64 B per tile: 16 MiB at n = 30; if the buffers cannot be allocated the
+    // sweep builds each tile's basis itself, as before)
     const size_t need = (size_t)kBasisEntryBytes * (size_t)a.ntiles;
     if (c->d_basis_cap < need) {
       if (c->d_basis) cudaFree(c->d_basis);
       c->d_basis = nullptr;
       c->d_basis_cap = 0;
-      CUDA_TRY(cudaMalloc(&c->d_basis, need));
-      c->d_basis_cap = need;
+      if (cudaMalloc(&c->d_basis, need) == cudaSuccess) c->d_basis_cap = need;
+      else { c->d_basis = nullptr; cudaGetLastError(); }
     }
     if (c->d_gen_tab_cap < te) {
       if (c->d_gen_tab) cudaFree(c->d_gen_tab);
       c->d_gen_tab = nullptr;
       c->d_gen_tab_cap = 0;
-      CUDA_TRY(cudaMalloc(&c->d_gen_tab, sizeof(double2) * (size_t)te));
-      c->d_gen_tab_cap = te;
+      if (cudaMalloc(&c->d_gen_tab, sizeof(double2) * (size_t)te) == cudaSuccess) c->d_gen_tab_cap = te;
+      else { c->d_gen_tab = nullptr; cudaGetLastError(); }
     }
-    CUDA_TRY(launch_gen_aux(a, c->d_basis, c->d_gen_tab, c->stream));
-    a.basis_tab = c->d_basis;
-    a.table = c->d_gen_tab;
-    a.flags = fl | kGenTab;
+    if (c->d_basis && c->d_gen_tab) {
+      CUDA_TRY(launch_gen_aux(a, c->d_basis, c->d_gen_tab, c->stream));
+      a.basis_tab = c->d_basis;
+      a.table = c->d_gen_tab;
+      a.flags = fl | kGenTab;
+    }
   }
   CUDA_TRY(launch_sweep(a, R.grid, c->stream));
   ++c->last_launches;
