@@ -761,6 +761,7 @@ int launch_plan_sweep(qaoa_ctx* c, int i, int64_t lo, int64_t cnt) {
     }
     if (c->d_basis && c->d_gen_tab) {
       CUDA_TRY(launch_gen_aux(a, c->d_basis, c->d_gen_tab, c->stream));
+      c->last_launches += 2;  // basis_table_kernel + gen_table_kernel
       a.basis_tab = c->d_basis;
       a.table = c->d_gen_tab;
       a.flags = fl | kGenTab;

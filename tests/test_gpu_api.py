@@ -199,7 +199,9 @@ def test_new_entry_points_reject_bad_arguments():
 
 
 def test_plan_export_matches_engine_launch_count():
-    """qaoa_plan (device-free) is the plan the engine runs: same sweep count."""
+    """qaoa_plan (device-free) is the plan the engine runs: same sweep count (the
+    engine's launch count adds the two launch-control helpers, basis_table_kernel
+    and gen_table_kernel)."""
     import ctypes
 
     from paper_2312_03019_b200 import _lib
@@ -213,7 +215,8 @@ def test_plan_export_matches_engine_launch_count():
         eng.call("qaoa_run_layers", 10, _lib.dptr(t.view(np.float64)), _lib.dptr(cs), _lib.dptr(ss), 0)
         nl, hb = ctypes.c_int(), ctypes.c_double()
         _lib.load().qaoa_last_run_stats(eng.ptr, ctypes.byref(nl), ctypes.byref(hb))
-        assert nl.value == _lib.load().qaoa_plan(30, 10, 0, None, 0) == 21
+        assert _lib.load().qaoa_plan(30, 10, 0, None, 0) == 21
+        assert nl.value == 21 + 2
     finally:
         eng.close()
 
