@@ -474,6 +474,7 @@ cudaError_t launch_sweep(const SweepArgs& a0, int grid, cudaStream_t stream) {
       if (!make_tile_map(&a.map, a.amps, n, a.carry, a.q)) return cudaErrorInvalidValue;
     }
   }
+  if (sweep32_selected(a)) return launch_sweep32(a, grid, stream);
   const int n_tables = ((a.flags & kPreCost) ? 1 : 0) + ((a.flags & kStage2) ? 1 : 0);
   const size_t smem = sweep_smem_bytes(n_tables * a.table_len);
   return a.g.n_nodes > 32 ? launch_w<true>(a, grid, smem, stream)

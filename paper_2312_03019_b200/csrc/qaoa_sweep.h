@@ -92,6 +92,12 @@ bool sweep_uses_tma(const SweepArgs& a);
 void set_sweep_impl(int v);  // force 0 / 1 / 2, or 3 = per-sweep policy (default); tooling / A-B tests
 int sweep_grid(const SweepArgs& a);
 cudaError_t launch_sweep_tma(const SweepArgs& a, cudaStream_t stream);
+// 128 x 32 register geometry for the fast C = 3 sweeps (qaoa_sweep32.cu); the
+// policy routes every eligible sweep there (one tile per CTA, like impl 0).
+bool sweep32_eligible(const SweepArgs& a);
+bool sweep32_selected(const SweepArgs& a);
+void set_sweep32(int on);  // -1: QAOA_SWEEP32 (default on), 0 off, 1 on
+cudaError_t launch_sweep32(const SweepArgs& a, int grid, cudaStream_t stream);
 cudaError_t launch_sweep(const SweepArgs& args, int grid, cudaStream_t stream);
 
 // simple (per-gate / per-element) kernels, qaoa_gates.cu

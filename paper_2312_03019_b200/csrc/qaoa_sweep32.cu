@@ -1,0 +1,298 @@
+// qaoa_sweep32.cu -- the fused sweep for the strided C = 3 sets (9 mixed
+// qubits: N = 30's level-boundary merged sweeps and its last sweep with <C>)
+// with 128 threads x 32 amplitudes per 4096-amplitude tile, two CTAs per SM.
+//
+// Why a second register geometry: in the 256 x 16 kernel (qaoa_sweep.cu) the
+// 9 mixed tile bits need three register windows (4 + 4 + 1), i.e. per merged
+// sweep two exchanges over 8 warps plus two lane transposes; the L1/shared
+// pipe is its busiest resource (62%, profiles/r10_summary.md).  Five-bit
+// register windows cover the 9 bits with two windows:
+//   ML: registers = tile bits 7..11, threads = tile bits 0..6        (HBM load/store)
+//   MB: registers = tile bits 3..7,  threads = tile bits 0..2, 8..11  (HBM store, FLOW 1)
+// (tile bit 7 rides along in MB unmixed: it is mixed in ML).  A merged sweep is
+// ML -> MB, cost, MB -> ML: two exchanges over 4 warps, no lane transposes (-11%
+// L1 wavefronts per tile).  Both mappings keep the carried bits 0..2 on lanes
+// 0..2, so every HBM access is a 128-byte run (four per warp instruction, as in
+// qaoa_sweep.cu) and every 8-lane phase of a 128-bit shared access covers 8
+// consecutive slots (conflict-free without padding).  255 registers per thread;
+// three CTAs per SM (168 registers) spill and measured slower.
+//
+// Arithmetic per amplitude: the fast-mode butterflies (rx_form1), the cost
+// lookup (cmul_np with the even phase table), scale and <C> of fast_tile; only
+// the order in which the nine qubits of a set are applied differs from the
+// 256 x 16 flow (~1e-15; the fast schedule's tolerance is 1e-12).  Exact,
+// weighted, mirror and launch-control sweeps keep the 256 x 16 kernels.
+//
+// Measured on B200 (tools/s32_probe.sh, profiles/r11_s32_probe.txt; policy with
+// vs without this kernel): merged sweep of set 1 6.48-6.50 vs 6.72 ms, of the top
+// set 7.28-7.30 vs 7.61-7.62, single / last sweeps unchanged (5.35-5.39 vs
+// 5.38-5.42); bench step 81.9-82.1 vs 80.4-80.6 layers/s (profiles/r11_s32_bench_ab.txt).
+//
+// Reference path replaced: see qaoa_sweep.cu (cost.py:162-176, circuit.py:89-94,
+// state.py:110-128, circuit.py:116-121).
+#include <stdlib.h>
+
+#include "qaoa_common.cuh"
+#include "qaoa_sweep.h"
+#include "qaoa_tile.cuh"
+
+namespace qb {
+namespace s32 {
+
+constexpr int kT = 128;
+constexpr int kR = 32;
+
+template <int M>
+__host__ __device__ constexpr int tidx(int tid, int r) {
+  return M == 0 ? (tid | (r << 7)) : ((tid & 7) | ((tid >> 3) << 8) | (r << 3));
+}
+template <int M>
+__host__ __device__ constexpr int rbit(int j) {  // tile bit of register bit j
+  return M == 0 ? 7 + j : 3 + j;
+}
+
+template <int A, int B>
+__device__ __forceinline__ void xchg(double2* buf, int tid, double2 (&v)[kR]) {
+#pragma unroll
+  for (int r = 0; r < kR; ++r) buf[tidx<A>(tid, r)] = v[r];
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kR; ++r) v[r] = buf[tidx<B>(tid, r)];
+}
+
+template <unsigned MASK>
+__device__ __forceinline__ void rx5(double2 (&v)[kR], double t) {
+#pragma unroll
+  for (int K = 0; K < 5; ++K) {
+    if (!((MASK >> K) & 1)) continue;
+#pragma unroll
+    for (int r = 0; r < kR; ++r)
+      if (!(r & (1 << K))) rx_form1(v[r], v[r | (1 << K)], t);
+  }
+}
+
+// Cut counts of the 32 registers of mapping M, produced in two halves of 16
+// (registers 0..15, then 16..31 = the first half with register bit 4 flipped)
+// so only 16 counts are live next to the 128 data registers.
+template <int M>
+struct Cut32 {
+  int c0, d[5], al[5], sg[5];
+  __device__ __forceinline__ Cut32(const CutBasis* cb, int tid) {
+    int pk[12];
+    const int4* p4 = reinterpret_cast<const int4*>(cb->pk);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int4 w = p4[i];
+      pk[4 * i] = w.x; pk[4 * i + 1] = w.y; pk[4 * i + 2] = w.z; pk[4 * i + 3] = w.w;
+    }
+    const int2 kt = *reinterpret_cast<const int2*>(&cb->K);
+    const int T = tidx<M>(tid, 0) ^ kt.y;
+    c0 = kt.x;
+#pragma unroll
+    for (int k = 0; k < 12; ++k)
+      if ((T >> k) & 1) c0 += (pk[k] >> 16) - __popc(pk[k] & T);
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const int b = rbit<M>(j);
+      al[j] = pk[b] & 0xFFF;
+      sg[j] = ((T >> b) & 1) ? -1 : 1;
+      d[j] = sg[j] * ((pk[b] >> 16) - 2 * __popc(al[j] & T));
+    }
+  }
+  __device__ __forceinline__ int a(int k, int j) const {  // k < j
+    return 2 * sg[k] * sg[j] * ((al[k] >> rbit<M>(j)) & 1);
+  }
+  // c[r], r < 16
+  __device__ __forceinline__ void low(int (&c)[16]) const {
+    c[0] = c0;
+#pragma unroll
+    for (int r = 1; r < 16; ++r) {
+      const int j = r >= 8 ? 3 : r >= 4 ? 2 : r >= 2 ? 1 : 0;
+      const int rest = r ^ (1 << j);
+      int v = c[rest] + d[j];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < j && ((rest >> k) & 1)) v -= a(k, j);
+      c[r] = v;
+    }
+  }
+  // c[r] -> c[r | 16]
+  __device__ __forceinline__ void high(int (&c)[16]) const {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      int v = c[r] + d[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((r >> k) & 1) v -= a(k, 4);
+      c[r] = v;
+    }
+  }
+};
+
+template <int M>
+__device__ __forceinline__ void cost32(double2 (&v)[kR], const CutBasis* cb, const double2* __restrict__ tab,
+                                       int e, int tid) {
+  const Cut32<M> cp(cb, tid);
+  int c[16];
+  cp.low(c);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = cmul_np(v[r], ld_phase(tab + (e - c[r])));
+  cp.high(c);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[16 + r] = cmul_np(v[16 + r], ld_phase(tab + (e - c[r])));
+}
+
+template <int M>
+__device__ __forceinline__ double expect32(const double2 (&v)[kR], const CutBasis* cb, int tid) {
+  const Cut32<M> cp(cb, tid);
+  int c[16];
+  cp.low(c);
+  double acc = 0.0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) acc += (v[r].x * v[r].x + v[r].y * v[r].y) * (double)c[r];
+  cp.high(c);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) acc += (v[16 + r].x * v[16 + r].x + v[16 + r].y * v[16 + r].y) * (double)c[r];
+  return acc;
+}
+
+}  // namespace s32
+
+#ifndef S32_MINB
+#define S32_MINB 2  // CTAs per SM (probe builds may try 3)
+#endif
+template <bool WIDE, int FLOW>
+__global__ void __launch_bounds__(s32::kT, S32_MINB) sweep32_kernel(const __grid_constant__ SweepArgs a) {
+  using namespace s32;
+  extern __shared__ __align__(16) unsigned char smem_raw32[];
+  double2* buf = reinterpret_cast<double2*>(smem_raw32);
+  __shared__ CutBasis cb;
+  __shared__ double red_scratch[kT / 32];
+  constexpr int C = 3;
+  const uint32_t flags = a.flags;
+  const int tid = threadIdx.x;
+  const int q = a.q;
+  const uint64_t Q = 1ull << q;
+  const uint64_t tile = (uint64_t)a.tile_lo + blockIdx.x;
+  const uint64_t base = tile_base<C>(tile, q);
+  double2* __restrict__ amps = a.amps;
+  // ML: thread part (t & 7) + (t >> 3) Q, register r adds (r << 4) Q
+  const uint64_t toff = (uint64_t)(tid & 7) + (uint64_t)(tid >> 3) * Q;
+  const uint64_t rs = 16ull * Q;
+
+  double2 v[kR];
+  if (flags & kGen) {
+#pragma unroll
+    for (int r = 0; r < kR; ++r) v[r] = a.gen;
+  } else {
+    const uint64_t pf_b = (uint64_t)a.tile_lo + blockIdx.x + a.pf_dist;
+    if (a.pf_dist > 0 && pf_b < (uint64_t)(a.tile_lo + (a.tile_cnt ? a.tile_cnt : a.ntiles))) {
+      if (!a.pf_tensor) {
+        prefetch_tile_l2<C, kT>(amps, tile_base<C>(pf_b, q), Q, tid);
+      } else if (tid == 0) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int c[5];
+          half_coords<C>(a, pf_b, h, c);
+          asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                           reinterpret_cast<uint64_t>(&a.map)),
+                       "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4])
+                       : "memory");
+        }
+      }
+    }
+    const double2* p = amps + base + toff;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) v[r] = ld_tile(p + r * rs);
+  }
+  const bool need_cut = flags & (kPreCost | kMidCost | kExpect);
+  if (need_cut) {
+    if (tid < 32) cut_basis<WIDE, C>(a, base, q, &cb);
+    if (flags & kPreCost) __syncthreads();
+  }
+  const int e = a.g.tot_edge;
+  const double t1 = a.rx1.a, t2 = a.rx2.a;
+  if (flags & kPreCost) cost32<0>(v, &cb, a.table, e, tid);
+  rx5<0x1Fu>(v, t1);
+  xchg<0, 1>(buf, tid, v);
+  rx5<0x0Fu>(v, t1);  // tile bits 3..6 (register bit 4 = tile bit 7, mixed in ML)
+  if (FLOW == 2) {
+    cost32<1>(v, &cb, a.table2, e, tid);
+    rx5<0x0Fu>(v, t2);
+  }
+  double acc = 0.0;
+  if (FLOW == 2) {
+    xchg<1, 0>(buf, tid, v);
+    rx5<0x1Fu>(v, t2);
+  }
+  constexpr int last = FLOW == 2 ? 0 : 1;
+  if (flags & kScale) {
+#pragma unroll
+    for (int r = 0; r < kR; ++r) v[r] = cmul_np(v[r], a.scale);
+  }
+  if (flags & kExpect) acc = expect32<last>(v, &cb, tid);
+  if (!(flags & kNoStore)) {
+    if (last == 0) {
+      double2* p = amps + base + toff;
+#pragma unroll
+      for (int r = 0; r < kR; ++r) __stcs(p + r * rs, v[r]);
+    } else {
+      // MB: tile index (tid & 7) | (tid >> 3) << 8 | r << 3 -> register stride Q
+      double2* p = amps + base + (uint64_t)(tid & 7) + (uint64_t)((tid >> 3) << 5) * Q;
+#pragma unroll
+      for (int r = 0; r < kR; ++r) __stcs(p + (uint64_t)r * Q, v[r]);
+    }
+  }
+  if (flags & kExpect) {
+    const double t = block_sum<kT>(acc, red_scratch);
+    if (threadIdx.x == 0) a.partials[tile] = t;
+  }
+}
+
+bool sweep32_eligible(const SweepArgs& a) {
+  return a.carry == 3 && !(a.flags & (kExact | kWeighted | kMirror | kGen)) && !a.out && a.ntiles >= 1 &&
+         (a.flags & kStage1);
+}
+
+static int g_sweep32 = -1;
+void set_sweep32(int on) { g_sweep32 = on; }
+
+// QAOA_SWEEP32=0 (or set_sweep32(0)) keeps every sweep on the 256 x 16 kernels (A/B).
+bool sweep32_selected(const SweepArgs& a) {
+  int on = g_sweep32;
+  if (on < 0) {
+    static int env = -2;
+    if (env == -2) {
+      const char* e = getenv("QAOA_SWEEP32");
+      env = e ? atoi(e) : 1;
+    }
+    on = env;
+  }
+  return on > 0 && sweep32_eligible(a);
+}
+
+template <bool WIDE, int FLOW>
+static cudaError_t launch32_one(const SweepArgs& a, int grid, cudaStream_t s) {
+  constexpr int smem = kTile * (int)sizeof(double2);
+  static unsigned long long configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(sweep32_kernel<WIDE, FLOW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem);
+    if (e != cudaSuccess) return e;
+    __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
+  }
+  sweep32_kernel<WIDE, FLOW><<<grid, s32::kT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sweep32(const SweepArgs& a, int grid, cudaStream_t s) {
+  if (!sweep32_eligible(a)) return cudaErrorNotSupported;
+  const bool f2 = a.flags & kStage2;
+  if (a.g.n_nodes > 32) return f2 ? launch32_one<true, 2>(a, grid, s) : launch32_one<true, 1>(a, grid, s);
+  return f2 ? launch32_one<false, 2>(a, grid, s) : launch32_one<false, 1>(a, grid, s);
+}
+
+}  // namespace qb

@@ -463,6 +463,7 @@ int sweep_impl(const SweepArgs& a) {
   if ((a.flags & (kExact | kWeighted | kMirror)) || a.carry == 11 || a.ntiles < 1 || a.out) return 0;
   const int env = impl_env();
   if (env != 3) return env;
+  if (sweep32_selected(a)) return 0;  // one tile per CTA, 128 x 32 (qaoa_sweep32.cu)
   if (a.flags & kGen) {  // QAOA_GEN_IMPL overrides for launch control only (A/B)
     static int gi = -2;
     if (gi == -2) {

@@ -4,7 +4,7 @@
 // on-chip work: FP64 butterflies, shared-memory exchanges, cut counts).
 //   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -std=c++17 --expt-relaxed-constexpr \
 //        -I paper_2312_03019_b200/csrc tools/sweep_probe.cu \
-//        paper_2312_03019_b200/csrc/qaoa_sweep.cu paper_2312_03019_b200/csrc/qaoa_sweep_tma.cu \
+//        paper_2312_03019_b200/csrc/qaoa_sweep.cu paper_2312_03019_b200/csrc/qaoa_sweep32.cu paper_2312_03019_b200/csrc/qaoa_sweep_tma.cu \
 //        paper_2312_03019_b200/csrc/qaoa_cut_table.cu -o tools/sweep_probe
 #include <cuda_runtime.h>
 #include <stdio.h>
@@ -14,6 +14,7 @@
 #include "qaoa_sweep.h"
 
 using namespace qb;
+
 
 static float time_sweep(const SweepArgs& a, int grid, int reps) {
   cudaEvent_t e0, e1;
@@ -93,7 +94,9 @@ static int check_mode(int n_lo, int n_hi, int other) {
           double2* y = impl ? y5 : y4;
           cudaMemcpy(y, x, 16 * size, cudaMemcpyDeviceToDevice);
           a.amps = y;
-          set_sweep_impl(impl ? other : 0);
+          // other == 32: the 128 x 32 C = 3 kernel against the 256 x 16 one
+          set_sweep32(impl && other == 32 ? 1 : 0);
+          set_sweep_impl(impl ? (other == 32 ? 0 : other) : 0);
           launch_sweep(a, (int)a.ntiles, 0);
           cudaError_t err = cudaDeviceSynchronize();
           if (err != cudaSuccess) { printf("n=%d error %s\n", n, cudaGetErrorString(err)); return 1; }
@@ -110,14 +113,15 @@ static int check_mode(int n_lo, int n_hi, int other) {
         double md = 0; uint64_t arg = 0, nbad = 0;
         for (uint64_t i = 0; i < size; ++i) {
           double d = fabs(h4[i].x - h[i].x) + fabs(h4[i].y - h[i].y);
-          if (d > 0) {
+          if (d > (other == 32 ? 1e-13 : 0.0)) {
             if (nbad < 8) printf("   diff at %llu (tile-internal 0x%03llx)\n", (unsigned long long)i, (unsigned long long)(i & 4095));
             ++nbad;
           }
           if (d > md) { md = d; arg = i; }
         }
         if (nbad) printf("   %llu differing amplitudes\n", (unsigned long long)nbad);
-        const bool ok = md == 0.0 && fabs(e4 - e5) <= 1e-12 * fabs(e4);
+        // the 128 x 32 experiment (other == 32) applies a set's qubits in another order
+        const bool ok = md <= (other == 32 ? 1e-13 : 0.0) && fabs(e4 - e5) <= 1e-12 * fabs(e4);
         bad += !ok;
         printf("n=%d set C=%2d q=%2d flags=0x%03x maxdiff=%.3e (at %llu) expect %.15g vs %.15g %s\n", n, carry[si], qs[si], fl, md,
                (unsigned long long)arg, e4, e5, ok ? "OK" : "FAIL");
@@ -322,7 +326,9 @@ int main(int argc, char** argv) {
       custom.flags = (uint32_t)strtol(argv[7], nullptr, 0);
     }
     const Kind& k = strcmp(argv[4], "custom") == 0 ? custom : kinds[atoi(argv[4])];
-    set_sweep_impl(impl);
+    // impl 30: the per-sweep policy without the 128 x 32 C = 3 kernel
+    set_sweep32(impl == 30 ? 0 : -1);
+    set_sweep_impl(impl == 30 ? 3 : impl);
     SweepArgs a;
     memset(&a, 0, sizeof(a));
     a.amps = amps; a.table = tab; a.table2 = tab + (E + 1); a.partials = partials; a.g = g;
