@@ -1,12 +1,15 @@
-// qaoa_sweep32.cu -- the fused sweep for the strided C = 3 sets (9 mixed
-// qubits: N = 30's level-boundary merged sweeps and its last sweep with <C>)
-// with 128 threads x 32 amplitudes per 4096-amplitude tile, two CTAs per SM.
+// qaoa_sweep32.cu -- the fused sweep for the strided sets with C = 3..7
+// carried bits (9..5 mixed qubits; the policy is in sweep32_eligible: N = 30's
+// merged and last sweeps, single sweeps of N = 33 / 26 / 24 / 28, every sweep
+// of the 5-qubit sets of N = 22) with 128 threads x 32 amplitudes
+// per 4096-amplitude tile, two CTAs per SM.
 //
 // Why a second register geometry: in the 256 x 16 kernel (qaoa_sweep.cu) the
-// 9 mixed tile bits need three register windows (4 + 4 + 1), i.e. per merged
-// sweep two exchanges over 8 warps plus two lane transposes; the L1/shared
-// pipe is its busiest resource (62%, profiles/r10_summary.md).  Five-bit
-// register windows cover the 9 bits with two windows:
+// 9 mixed tile bits of a C = 3 set need three register windows (4 + 4 + 1),
+// i.e. per merged sweep two exchanges over 8 warps plus two lane transposes;
+// the L1/shared pipe is its busiest resource (62%, profiles/r10_summary.md).
+// Five-bit register windows cover the mixed bits with at most two windows
+// (for C = 7 the load window alone: no exchange):
 //   ML: registers = tile bits 7..11, threads = tile bits 0..6        (HBM load/store)
 //   MB: registers = tile bits 3..7,  threads = tile bits 0..2, 8..11  (HBM store, FLOW 1)
 // (tile bit 7 rides along in MB unmixed: it is mixed in ML).  A merged sweep is
@@ -161,14 +164,33 @@ __device__ __forceinline__ double expect32(const double2 (&v)[kR], const CutBasi
 #ifndef S32_MINB
 #define S32_MINB 2  // CTAs per SM (probe builds may try 3)
 #endif
-template <bool WIDE, int FLOW>
+
+namespace s32 {
+// Register-bit masks of the two windows for carried-bit count C (3 <= C <= 7):
+// ML mixes tile bits 7..11 (all >= C); MB mixes its tile bits 3..6 that are >= C.
+template <int C>
+__host__ __device__ constexpr unsigned mask_mb() {
+  return (0xFu >> (C > 3 ? C - 3 : 0)) << (C > 3 ? C - 3 : 0) & 0xFu;
+}
+// Physical offset of tile index t (tile_off<C> without the loop): the carried
+// bits stay, the mixed bits scale by Q; linear over disjoint bit fields.
+template <int C>
+__device__ __forceinline__ uint64_t off(int t, uint64_t Q) {
+  return (uint64_t)(t & ((1 << C) - 1)) + (uint64_t)(t >> C) * Q;
+}
+}  // namespace s32
+
+// FLOW 1: [cost] RX(set); FLOW 2: [cost] RX(set) -> cost -> RX(set).  Fast
+// schedule, unweighted, in place, 3 <= C <= 7, never launch control.
+template <bool WIDE, int C, int FLOW>
 __global__ void __launch_bounds__(s32::kT, S32_MINB) sweep32_kernel(const __grid_constant__ SweepArgs a) {
   using namespace s32;
+  static_assert(C >= 3 && C <= 7, "C = 3..7");
+  constexpr unsigned kMB = mask_mb<C>();  // 0 for C = 7: ML alone holds every mixed bit
   extern __shared__ __align__(16) unsigned char smem_raw32[];
   double2* buf = reinterpret_cast<double2*>(smem_raw32);
-  __shared__ CutBasis cb;
+  __shared__ CutBasis cb_s;
   __shared__ double red_scratch[kT / 32];
-  constexpr int C = 3;
   const uint32_t flags = a.flags;
   const int tid = threadIdx.x;
   const int q = a.q;
@@ -176,11 +198,12 @@ __global__ void __launch_bounds__(s32::kT, S32_MINB) sweep32_kernel(const __grid
   const uint64_t tile = (uint64_t)a.tile_lo + blockIdx.x;
   const uint64_t base = tile_base<C>(tile, q);
   double2* __restrict__ amps = a.amps;
-  // ML: thread part (t & 7) + (t >> 3) Q, register r adds (r << 4) Q
-  const uint64_t toff = (uint64_t)(tid & 7) + (uint64_t)(tid >> 3) * Q;
-  const uint64_t rs = 16ull * Q;
+  const uint64_t toff = off<C>(tidx<0>(tid, 0), Q);  // ML thread part
+  const uint64_t rs = Q << (7 - C);                    // ML register stride (tile bit 7)
 
   double2 v[kR];
+  // (the policy never sends launch control here, but without this branch around
+  // the loads ptxas spills 96 bytes in the C = 3 merged flow)
   if (flags & kGen) {
 #pragma unroll
     for (int r = 0; r < kR; ++r) v[r] = a.gen;
@@ -205,42 +228,47 @@ __global__ void __launch_bounds__(s32::kT, S32_MINB) sweep32_kernel(const __grid
 #pragma unroll
     for (int r = 0; r < kR; ++r) v[r] = ld_tile(p + r * rs);
   }
+  // the tile's cut basis, built by warp 0 and published by the first barrier
+  const CutBasis* cb = &cb_s;
   const bool need_cut = flags & (kPreCost | kMidCost | kExpect);
   if (need_cut) {
-    if (tid < 32) cut_basis<WIDE, C>(a, base, q, &cb);
-    if (flags & kPreCost) __syncthreads();
+    if (tid < 32) cut_basis<WIDE, C>(a, base, q, &cb_s);
+    if ((flags & kPreCost) || kMB == 0) __syncthreads();
   }
   const int e = a.g.tot_edge;
   const double t1 = a.rx1.a, t2 = a.rx2.a;
-  if (flags & kPreCost) cost32<0>(v, &cb, a.table, e, tid);
+  if (flags & kPreCost) cost32<0>(v, cb, a.table, e, tid);
   rx5<0x1Fu>(v, t1);
-  xchg<0, 1>(buf, tid, v);
-  rx5<0x0Fu>(v, t1);  // tile bits 3..6 (register bit 4 = tile bit 7, mixed in ML)
-  if (FLOW == 2) {
-    cost32<1>(v, &cb, a.table2, e, tid);
-    rx5<0x0Fu>(v, t2);
+  if (kMB) {
+    xchg<0, 1>(buf, tid, v);
+    rx5<kMB>(v, t1);
   }
-  double acc = 0.0;
   if (FLOW == 2) {
-    xchg<1, 0>(buf, tid, v);
+    if (kMB) {
+      cost32<1>(v, cb, a.table2, e, tid);
+      rx5<kMB>(v, t2);
+      xchg<1, 0>(buf, tid, v);
+    } else {
+      cost32<0>(v, cb, a.table2, e, tid);
+    }
     rx5<0x1Fu>(v, t2);
   }
-  constexpr int last = FLOW == 2 ? 0 : 1;
+  constexpr int last = (FLOW == 2 || !kMB) ? 0 : 1;
   if (flags & kScale) {
 #pragma unroll
     for (int r = 0; r < kR; ++r) v[r] = cmul_np(v[r], a.scale);
   }
-  if (flags & kExpect) acc = expect32<last>(v, &cb, tid);
+  double acc = 0.0;
+  if (flags & kExpect) acc = expect32<last>(v, cb, tid);
   if (!(flags & kNoStore)) {
     if (last == 0) {
       double2* p = amps + base + toff;
 #pragma unroll
       for (int r = 0; r < kR; ++r) __stcs(p + r * rs, v[r]);
     } else {
-      // MB: tile index (tid & 7) | (tid >> 3) << 8 | r << 3 -> register stride Q
-      double2* p = amps + base + (uint64_t)(tid & 7) + (uint64_t)((tid >> 3) << 5) * Q;
+      double2* p = amps + base + off<C>(tidx<1>(tid, 0), Q);
 #pragma unroll
-      for (int r = 0; r < kR; ++r) __stcs(p + (uint64_t)r * Q, v[r]);
+      for (int r = 0; r < kR; ++r) __stcs(p + off<C>(tidx<1>(0, r), Q), v[r]);
     }
   }
   if (flags & kExpect) {
@@ -249,15 +277,29 @@ __global__ void __launch_bounds__(s32::kT, S32_MINB) sweep32_kernel(const __grid
   }
 }
 
+// Where the 128 x 32 geometry measured faster (tools/s32_probe2.sh,
+// tools/s32_policy_ab.sh, tools/c456_probe.sh; profiles/r11_s32_*):
+// * every C = 3 sweep (two windows instead of 4 + 4 + 1);
+// * every C = 7 sweep (the load window holds all 5 mixed bits: no exchange;
+//   merged 5.34 vs 6.21 ms, N=22 p=4 +3.7%);
+// * the single-stage sweeps of C = 4..6 (one exchange either way; N=33 single
+//   42.4 vs 44.8 ms, last sweep + <C> 49.1 vs 51.3; N=33 step +1.1%).
+// C = 4..6 merged sweeps need two exchanges either way and are as fast or faster
+// on 16 warps per SM (C = 4: 6.51 vs 6.77 ms, C = 5: 6.48 vs 6.59, C = 6: 6.37
+// vs 6.40); launch control is faster on the TMA in/out kernel (3.96 vs 4.29).
+static bool sweep32_supported(const SweepArgs& a) {
+  return a.carry >= 3 && a.carry <= 7 && !(a.flags & (kExact | kWeighted | kMirror | kGen)) && !a.out &&
+         a.ntiles >= 1 && (a.flags & kStage1);
+}
 bool sweep32_eligible(const SweepArgs& a) {
-  return a.carry == 3 && !(a.flags & (kExact | kWeighted | kMirror | kGen)) && !a.out && a.ntiles >= 1 &&
-         (a.flags & kStage1);
+  return sweep32_supported(a) && (a.carry == 3 || a.carry == 7 || !(a.flags & kStage2));
 }
 
 static int g_sweep32 = -1;
 void set_sweep32(int on) { g_sweep32 = on; }
 
-// QAOA_SWEEP32=0 (or set_sweep32(0)) keeps every sweep on the 256 x 16 kernels (A/B).
+// QAOA_SWEEP32=0 (or set_sweep32(0)) keeps every sweep on the 256 x 16 kernels,
+// QAOA_SWEEP32=2 sends every supported sweep here (A/B only).
 bool sweep32_selected(const SweepArgs& a) {
   int on = g_sweep32;
   if (on < 0) {
@@ -268,10 +310,10 @@ bool sweep32_selected(const SweepArgs& a) {
     }
     on = env;
   }
-  return on > 0 && sweep32_eligible(a);
+  return on == 2 ? sweep32_supported(a) : (on > 0 && sweep32_eligible(a));
 }
 
-template <bool WIDE, int FLOW>
+template <bool WIDE, int C, int FLOW>
 static cudaError_t launch32_one(const SweepArgs& a, int grid, cudaStream_t s) {
   constexpr int smem = kTile * (int)sizeof(double2);
   static unsigned long long configured = 0;
@@ -279,20 +321,35 @@ static cudaError_t launch32_one(const SweepArgs& a, int grid, cudaStream_t s) {
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(sweep32_kernel<WIDE, FLOW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(sweep32_kernel<WIDE, C, FLOW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          smem);
     if (e != cudaSuccess) return e;
     __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
   }
-  sweep32_kernel<WIDE, FLOW><<<grid, s32::kT, smem, s>>>(a);
+  sweep32_kernel<WIDE, C, FLOW><<<grid, s32::kT, smem, s>>>(a);
   return cudaGetLastError();
 }
 
+template <bool WIDE, int C>
+static cudaError_t launch32_c(const SweepArgs& a, int grid, cudaStream_t s) {
+  return (a.flags & kStage2) ? launch32_one<WIDE, C, 2>(a, grid, s) : launch32_one<WIDE, C, 1>(a, grid, s);
+}
+
+template <bool WIDE>
+static cudaError_t launch32_w(const SweepArgs& a, int grid, cudaStream_t s) {
+  switch (a.carry) {
+    case 3: return launch32_c<WIDE, 3>(a, grid, s);
+    case 4: return launch32_c<WIDE, 4>(a, grid, s);
+    case 5: return launch32_c<WIDE, 5>(a, grid, s);
+    case 6: return launch32_c<WIDE, 6>(a, grid, s);
+    case 7: return launch32_c<WIDE, 7>(a, grid, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
 cudaError_t launch_sweep32(const SweepArgs& a, int grid, cudaStream_t s) {
-  if (!sweep32_eligible(a)) return cudaErrorNotSupported;
-  const bool f2 = a.flags & kStage2;
-  if (a.g.n_nodes > 32) return f2 ? launch32_one<true, 2>(a, grid, s) : launch32_one<true, 1>(a, grid, s);
-  return f2 ? launch32_one<false, 2>(a, grid, s) : launch32_one<false, 1>(a, grid, s);
+  if (!sweep32_supported(a)) return cudaErrorNotSupported;
+  return a.g.n_nodes > 32 ? launch32_w<true>(a, grid, s) : launch32_w<false>(a, grid, s);
 }
 
 }  // namespace qb
