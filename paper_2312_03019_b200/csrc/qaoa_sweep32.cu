@@ -17,8 +17,8 @@
 // L1 wavefronts per tile).  Both mappings keep the carried bits 0..2 on lanes
 // 0..2, so every HBM access is a 128-byte run (four per warp instruction, as in
 // qaoa_sweep.cu) and every 8-lane phase of a 128-bit shared access covers 8
-// consecutive slots (conflict-free without padding).  255 registers per thread;
-// three CTAs per SM (168 registers) spill and measured slower.
+// consecutive slots (conflict-free without padding).  CTAs per SM: see
+// S32_MINB_F below.
 //
 // Arithmetic per amplitude: the fast-mode butterflies (rx_form1), the cost
 // lookup (cmul_np with the even phase table), scale and <C> of fast_tile; only
@@ -161,8 +161,16 @@ __device__ __forceinline__ double expect32(const double2 (&v)[kR], const CutBasi
 
 }  // namespace s32
 
+// CTAs per SM: C = 3 merged sweeps 3 (168 registers, 16-32 B of spills; merged
+// set-1 sweep 6.16 vs 6.50 ms with 2, bench step 83.1-83.3 vs 81.0-81.1
+// layers/s), everything else 2 (255 registers; single-stage sweeps 0.3-0.6%
+// and the C = 7 merged sweeps of N=22 2.4% faster than with 3) --
+// tools/ab_probe.sh, profiles/r12_minb_ab.txt, r12_minb_bench_ab.txt.
+// S32_MINB overrides all (probe builds).
 #ifndef S32_MINB
-#define S32_MINB 2  // CTAs per SM (probe builds may try 3)
+#define S32_MINB_F(C, FLOW) (((FLOW) == 2 && (C) == 3) ? 3 : 2)
+#else
+#define S32_MINB_F(C, FLOW) S32_MINB
 #endif
 
 namespace s32 {
@@ -183,7 +191,7 @@ __device__ __forceinline__ uint64_t off(int t, uint64_t Q) {
 // FLOW 1: [cost] RX(set); FLOW 2: [cost] RX(set) -> cost -> RX(set).  Fast
 // schedule, unweighted, in place, 3 <= C <= 7, never launch control.
 template <bool WIDE, int C, int FLOW>
-__global__ void __launch_bounds__(s32::kT, S32_MINB) sweep32_kernel(const __grid_constant__ SweepArgs a) {
+__global__ void __launch_bounds__(s32::kT, S32_MINB_F(C, FLOW)) sweep32_kernel(const __grid_constant__ SweepArgs a) {
   using namespace s32;
   static_assert(C >= 3 && C <= 7, "C = 3..7");
   constexpr unsigned kMB = mask_mb<C>();  // 0 for C = 7: ML alone holds every mixed bit
