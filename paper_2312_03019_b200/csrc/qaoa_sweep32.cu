@@ -161,14 +161,14 @@ __device__ __forceinline__ double expect32(const double2 (&v)[kR], const CutBasi
 
 }  // namespace s32
 
-// CTAs per SM: C = 3 merged sweeps 3 (168 registers, 16-32 B of spills; merged
-// set-1 sweep 6.16 vs 6.50 ms with 2, bench step 83.1-83.3 vs 81.0-81.1
-// layers/s), everything else 2 (255 registers; single-stage sweeps 0.3-0.6%
-// and the C = 7 merged sweeps of N=22 2.4% faster than with 3) --
-// tools/ab_probe.sh, profiles/r12_minb_ab.txt, r12_minb_bench_ab.txt.
+// CTAs per SM: merged sweeps of C = 3..6 run 3 (168 registers, 16-32 B of
+// spills; C = 3 set-1 merged sweep 6.16 vs 6.50 ms with 2, bench step 83.1-83.3
+// vs 81.0-81.1 layers/s), everything else 2 (255 registers; single-stage sweeps
+// 0.3-0.6% and the C = 7 merged sweeps of N=22 2.4% faster than with 3) --
+// tools/ab_probe.sh, tools/c456_m3_probe.sh, profiles/r12_minb_*.txt.
 // S32_MINB overrides all (probe builds).
 #ifndef S32_MINB
-#define S32_MINB_F(C, FLOW) (((FLOW) == 2 && (C) == 3) ? 3 : 2)
+#define S32_MINB_F(C, FLOW) (((FLOW) == 2 && (C) <= 6) ? 3 : 2)  // (merged C = 4..6 only via QAOA_SWEEP32=2)
 #else
 #define S32_MINB_F(C, FLOW) S32_MINB
 #endif
@@ -291,16 +291,22 @@ __global__ void __launch_bounds__(s32::kT, S32_MINB_F(C, FLOW)) sweep32_kernel(c
 // * every C = 7 sweep (the load window holds all 5 mixed bits: no exchange;
 //   merged 5.34 vs 6.21 ms, N=22 p=4 +3.7%);
 // * the single-stage sweeps of C = 4..6 (one exchange either way; N=33 single
-//   42.4 vs 44.8 ms, last sweep + <C> 49.1 vs 51.3; N=33 step +1.1%).
-// C = 4..6 merged sweeps need two exchanges either way and are as fast or faster
-// on 16 warps per SM (C = 4: 6.51 vs 6.77 ms, C = 5: 6.48 vs 6.59, C = 6: 6.37
-// vs 6.40); launch control is faster on the TMA in/out kernel (3.96 vs 4.29).
+//   42.4 vs 44.8 ms, last sweep + <C> 49.1 vs 51.3; N=33 step +1.1%);
+// C = 4..6 merged sweeps stay on 256 x 16 (see sweep32_eligible).  Launch
+// control is faster on the TMA in/out kernel (3.96 vs 4.29 ms).
 static bool sweep32_supported(const SweepArgs& a) {
   return a.carry >= 3 && a.carry <= 7 && !(a.flags & (kExact | kWeighted | kMirror | kGen)) && !a.out &&
          a.ntiles >= 1 && (a.flags & kStage1);
 }
 bool sweep32_eligible(const SweepArgs& a) {
-  return sweep32_supported(a) && (a.carry == 3 || a.carry == 7 || !(a.flags & kStage2));
+  if (!sweep32_supported(a)) return false;
+  // The choice depends on C and the flow only, never on the set's position: the
+  // swapped qubit layout moves merges between geometries and must stay bit for
+  // bit the in-place run.  (C = 4..6 merged sweeps at 3 CTAs per SM win where
+  // the tile spans <= 256 MB -- C = 4 5.87 vs 6.10 ms, C = 5 5.90 vs 6.07, C = 6
+  // 5.55 vs 5.95 -- and lose on a wide top set, C = 5 at q = 21 6.54 vs 6.15,
+  // profiles/r12_c456_m3.txt: a span rule would break that identity.)
+  return a.carry == 3 || a.carry == 7 || !(a.flags & kStage2);
 }
 
 static int g_sweep32 = -1;
