@@ -318,6 +318,32 @@ def sweep_kinds(L, n: int, p: int, exact: bool, count: int) -> list[str]:
     return kinds if len(kinds) == count else ["sweep"] * count
 
 
+def dominant_kernel_text(L, n: int, p: int, exact: bool, dom) -> str:
+    """Which kernel runs the dominant sweep kind (the policy of qaoa_sweep32.cu
+    sweep32_eligible / qaoa_sweep_tma.cu sweep_impl for the plan's geometry)."""
+    if not dom:
+        return "fused sweeps"
+    carry = None
+    buf = (ctypes.c_int * (7 * 256))()
+    ns = L.qaoa_plan(n, p, 1 if exact else 0, buf, 256)
+    for i in range(1, max(ns, 0)):
+        c, _q, _pre, _s1, mid = buf[7 * i:7 * i + 5]
+        if ("merged" in dom and mid >= 0) or ("low-set" in dom and c == 12) or \
+                ("last" in dom and i == ns - 1):
+            carry = c
+            break
+    s32 = (not exact and carry is not None and 3 <= carry <= 7 and os.environ.get("QAOA_SWEEP32", "1") != "0"
+           and (carry in (3, 7) or "merged" not in dom))
+    if s32:
+        ctas = "three" if ("merged" in dom and carry == 3) else "two"
+        xch = "no exchange" if carry == 7 else ("two exchanges" if "merged" in dom else "one exchange")
+        return (f"{dom}: qb::sweep32_kernel (128 threads x 32 amplitudes per 4096-amplitude tile, "
+                f"{ctas} CTAs per SM, L2 tile prefetch; five-bit register windows, {xch}, "
+                "no lane transposes; C = %d)" % carry)
+    return (f"{dom}: qb::sweep_kernel (256 threads x 16 amplitudes per 4096-amplitude tile, two CTAs "
+            "per SM, L2 tile prefetch)")
+
+
 def p1_closed_form(n: int, edges, gamma: float, beta: float) -> float:
     """<C> of a p=1 circuit on any unweighted graph, edge by edge (Wang, Hadfield,
     Jiang, Rieffel 2018, mapped to the reference's convention).
@@ -617,9 +643,7 @@ def run_ours(args, rank: int, world: int, local: int):
     roofline = {"bound": "hbm", "achieved": dk["GBps"], "peak": peak, "unit": "GB/s",
                 "frac": dk["frac"], "traffic": traffic if dom and "merged" in dom else None,
                 "peak_kind": peak_kind,
-                "kernel": f"{dom}: qb::sweep_kernel (one 4096-amplitude tile per CTA, two CTAs per "
-                          "SM, L2 tile prefetch; RX on both levels' set, the next level's cost "
-                          "between them)" if dom else "fused sweeps",
+                "kernel": dominant_kernel_text(L, n, p, args.exact, dom),
                 "algorithmic_bytes_per_launch": dk["algorithmic_bytes_per_launch"],
                 "avg_launch_ms": dk["avg_ms"],
                 "per_kind": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv)
