@@ -739,7 +739,7 @@ int launch_plan_sweep(qaoa_ctx* c, int i, int64_t lo, int64_t cnt) {
   if (last && R.expect_fused) fl |= kExpect;
   if (last && R.no_store_last) fl |= kNoStore;
   a.flags = fl;
-  if ((fl & kGen) && (fl & kPreCost) && sweep_uses_tma(a) && gen_aux_enabled()) {
+  if ((fl & kGen) && (fl & kPreCost) && (sweep_uses_tma(a) || sweep32_selected(a)) && gen_aux_enabled()) {
     // launch control on the TMA-fed kernel: tile bases built ahead (off the
     // per-tile critical path) and the uniform amplitude folded into the table
     // (64 B per tile: 16 MiB at n = 30; if the buffers cannot be allocated the

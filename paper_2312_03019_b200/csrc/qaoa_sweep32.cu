@@ -159,6 +159,21 @@ __device__ __forceinline__ double expect32(const double2 (&v)[kR], const CutBasi
   return acc;
 }
 
+// Launch control with the gen x phase table (kGenTab): every register starts
+// as gen, so the product is the table entry (as apply_gen_phase).
+template <int M>
+__device__ __forceinline__ void gen32(double2 (&v)[kR], const CutBasis* cb, const double2* __restrict__ gtab,
+                                      int e, int tid) {
+  const Cut32<M> cp(cb, tid);
+  int c[16];
+  cp.low(c);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = ld_phase(gtab + (e - c[r]));
+  cp.high(c);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[16 + r] = ld_phase(gtab + (e - c[r]));
+}
+
 }  // namespace s32
 
 // CTAs per SM: merged sweeps of C = 3..6 run 3 (168 registers, 16-32 B of
@@ -168,7 +183,7 @@ __device__ __forceinline__ double expect32(const double2 (&v)[kR], const CutBasi
 // tools/ab_probe.sh, tools/c456_m3_probe.sh, profiles/r12_minb_*.txt.
 // S32_MINB overrides all (probe builds).
 #ifndef S32_MINB
-#define S32_MINB_F(C, FLOW) (((FLOW) == 2 && (C) <= 6) ? 3 : 2)  // (merged C = 4..6 only via QAOA_SWEEP32=2)
+#define S32_MINB_F(C, FLOW) ((((FLOW) == 2 || (FLOW) == 3) && (C) <= 6) ? 3 : 2)  // (merged C = 4..6 only via QAOA_SWEEP32=2)
 #else
 #define S32_MINB_F(C, FLOW) S32_MINB
 #endif
@@ -236,16 +251,20 @@ __global__ void __launch_bounds__(s32::kT, S32_MINB_F(C, FLOW)) sweep32_kernel(c
 #pragma unroll
     for (int r = 0; r < kR; ++r) v[r] = ld_tile(p + r * rs);
   }
-  // the tile's cut basis, built by warp 0 and published by the first barrier
+  // the tile's cut basis: prebuilt (launch control, FLOW 3, launch_gen_aux) or
+  // built by warp 0 and published by the first barrier
   const CutBasis* cb = &cb_s;
   const bool need_cut = flags & (kPreCost | kMidCost | kExpect);
-  if (need_cut) {
+  if (FLOW == 3 && a.basis_tab) {
+    cb = reinterpret_cast<const CutBasis*>(a.basis_tab) + tile;
+  } else if (need_cut) {
     if (tid < 32) cut_basis<WIDE, C>(a, base, q, &cb_s);
     if ((flags & kPreCost) || kMB == 0) __syncthreads();
   }
   const int e = a.g.tot_edge;
   const double t1 = a.rx1.a, t2 = a.rx2.a;
-  if (flags & kPreCost) cost32<0>(v, cb, a.table, e, tid);
+  if (FLOW == 3 && (flags & kGenTab)) gen32<0>(v, cb, a.table, e, tid);
+  else if (flags & kPreCost) cost32<0>(v, cb, a.table, e, tid);
   rx5<0x1Fu>(v, t1);
   if (kMB) {
     xchg<0, 1>(buf, tid, v);
@@ -292,10 +311,24 @@ __global__ void __launch_bounds__(s32::kT, S32_MINB_F(C, FLOW)) sweep32_kernel(c
 //   merged 5.34 vs 6.21 ms, N=22 p=4 +3.7%);
 // * the single-stage sweeps of C = 4..6 (one exchange either way; N=33 single
 //   42.4 vs 44.8 ms, last sweep + <C> 49.1 vs 51.3; N=33 step +1.1%);
-// C = 4..6 merged sweeps stay on 256 x 16 (see sweep32_eligible).  Launch
-// control is faster on the TMA in/out kernel (3.96 vs 4.29 ms).
+// C = 4..6 merged sweeps stay on 256 x 16 (see sweep32_eligible); launch
+// control runs here with the prebuilt tile bases (gen32_enabled).
+// Launch control (FLOW 3) with the prebuilt tile bases and the gen x phase
+// table of launch_gen_aux, three CTAs per SM: 3.97 vs 4.37-4.40 ms on the TMA
+// in/out kernel inside the step (profiles/r12_gen32_ab.txt; without the helpers
+// and at two CTAs per SM it was slower, 4.29 vs 3.96 ms).  QAOA_SWEEP32_GEN=0
+// keeps it on the TMA kernel (A/B).
+static bool gen32_enabled() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("QAOA_SWEEP32_GEN");
+    v = e ? atoi(e) : 1;
+  }
+  return v > 0;
+}
 static bool sweep32_supported(const SweepArgs& a) {
-  return a.carry >= 3 && a.carry <= 7 && !(a.flags & (kExact | kWeighted | kMirror | kGen)) && !a.out &&
+  if ((a.flags & kGen) && (!gen32_enabled() || (a.flags & kStage2))) return false;
+  return a.carry >= 3 && a.carry <= 7 && !(a.flags & (kExact | kWeighted | kMirror)) && !a.out &&
          a.ntiles >= 1 && (a.flags & kStage1);
 }
 bool sweep32_eligible(const SweepArgs& a) {
@@ -346,6 +379,7 @@ static cudaError_t launch32_one(const SweepArgs& a, int grid, cudaStream_t s) {
 
 template <bool WIDE, int C>
 static cudaError_t launch32_c(const SweepArgs& a, int grid, cudaStream_t s) {
+  if (a.flags & kGen) return launch32_one<WIDE, C, 3>(a, grid, s);  // launch control (FLOW 1 + kGen)
   return (a.flags & kStage2) ? launch32_one<WIDE, C, 2>(a, grid, s) : launch32_one<WIDE, C, 1>(a, grid, s);
 }
 
