@@ -174,6 +174,67 @@ __device__ __forceinline__ void gen32(double2 (&v)[kR], const CutBasis* cb, cons
   for (int r = 0; r < 16; ++r) v[16 + r] = ld_phase(gtab + (e - c[r]));
 }
 
+// Weighted cost (compressed backend, fast schedule) on the 32 registers of
+// mapping M: the factored per-tile phase of qaoa_tile.cuh apply_wcost, register
+// combinations walked in Gray-code order over the five register bits.
+template <int M>
+__device__ __forceinline__ void wcost32(double2 (&v)[kR], const WBasis* wb, const double2* __restrict__ qt,
+                                        int tid) {
+  const int T = tidx<M>(tid, 0) ^ wb->tmask;
+  double2 cur = wb->F;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    const double2 b = wb->B[k];
+    cur = cmul_u(cur, ((T >> k) & 1) ? conj2(b) : b);
+  }
+  double2 up[5];  // multiplier when register bit j flips away from T's value
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    const double2 b = wb->B[rbit<M>(j)];
+    const double2 b2 = cmul_u(b, b);
+    up[j] = ((T >> rbit<M>(j)) & 1) ? b2 : conj2(b2);
+  }
+  int prev = 0;
+#pragma unroll
+  for (int k = 0; k < kR; ++k) {
+    const int r = k ^ (k >> 1);  // Gray order
+    if (k) {
+      const int x = r ^ prev;
+      const int j = x == 1 ? 0 : x == 2 ? 1 : x == 4 ? 2 : x == 8 ? 3 : 4;
+      cur = cmul_u(cur, ((r >> j) & 1) ? up[j] : conj2(up[j]));
+    }
+    prev = r;
+    const double2 ph = cmul_u(cur, __ldg(qt + ((T ^ tidx<M>(0, r)) & 0xFFF)));
+    v[r] = cmul_u(v[r], ph);
+  }
+}
+
+// Weighted <C> partial of the 32 registers of mapping M (qaoa_tile.cuh expect_wacc).
+template <int M>
+__device__ __forceinline__ double wexpect32(const double2 (&v)[kR], const WCutBasis* wb,
+                                            const double* __restrict__ cint, int tid) {
+  const int T = tidx<M>(tid, 0) ^ wb->tmask;
+  double base = wb->hh;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) base += ((T >> k) & 1) ? wb->W[k] - wb->S[k] : wb->S[k];
+  double d[5];
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    const double S = wb->S[rbit<M>(j)], W = wb->W[rbit<M>(j)];
+    d[j] = ((T >> rbit<M>(j)) & 1) ? 2.0 * S - W : W - 2.0 * S;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    double val = base + __ldg(cint + ((T ^ tidx<M>(0, r)) & 0xFFF));
+#pragma unroll
+    for (int j = 0; j < 5; ++j)
+      if ((r >> j) & 1) val += d[j];
+    acc += (v[r].x * v[r].x + v[r].y * v[r].y) * val;
+  }
+  return acc;
+}
+
 }  // namespace s32
 
 // CTAs per SM: merged sweeps of C = 3..6 run 3 (168 registers, 16-32 B of
@@ -183,9 +244,9 @@ __device__ __forceinline__ void gen32(double2 (&v)[kR], const CutBasis* cb, cons
 // tools/ab_probe.sh, tools/c456_m3_probe.sh, profiles/r12_minb_*.txt.
 // S32_MINB overrides all (probe builds).
 #ifndef S32_MINB
-#define S32_MINB_F(C, FLOW) ((((FLOW) == 2 || (FLOW) == 3) && (C) <= 6) ? 3 : 2)  // (merged C = 4..6 only via QAOA_SWEEP32=2)
+#define S32_MINB_F(C, FLOW, WGT) ((!(WGT) && ((FLOW) == 2 || (FLOW) == 3) && (C) <= 6) ? 3 : 2)  // (merged C = 4..6 only via QAOA_SWEEP32=2)
 #else
-#define S32_MINB_F(C, FLOW) S32_MINB
+#define S32_MINB_F(C, FLOW, WGT) S32_MINB
 #endif
 
 namespace s32 {
@@ -205,14 +266,16 @@ __device__ __forceinline__ uint64_t off(int t, uint64_t Q) {
 
 // FLOW 1: [cost] RX(set); FLOW 2: [cost] RX(set) -> cost -> RX(set).  Fast
 // schedule, unweighted, in place, 3 <= C <= 7, never launch control.
-template <bool WIDE, int C, int FLOW>
-__global__ void __launch_bounds__(s32::kT, S32_MINB_F(C, FLOW)) sweep32_kernel(const __grid_constant__ SweepArgs a) {
+template <bool WIDE, int C, int FLOW, bool WGT = false>
+__global__ void __launch_bounds__(s32::kT, S32_MINB_F(C, FLOW, WGT)) sweep32_kernel(const __grid_constant__ SweepArgs a) {
   using namespace s32;
   static_assert(C >= 3 && C <= 7, "C = 3..7");
   constexpr unsigned kMB = mask_mb<C>();  // 0 for C = 7: ML alone holds every mixed bit
   extern __shared__ __align__(16) unsigned char smem_raw32[];
   double2* buf = reinterpret_cast<double2*>(smem_raw32);
   __shared__ CutBasis cb_s;
+  __shared__ WBasis wb_s[WGT ? 2 : 1];
+  __shared__ WCutBasis wcb_s[WGT ? 1 : 1];
   __shared__ double red_scratch[kT / 32];
   const uint32_t flags = a.flags;
   const int tid = threadIdx.x;
@@ -258,12 +321,21 @@ __global__ void __launch_bounds__(s32::kT, S32_MINB_F(C, FLOW)) sweep32_kernel(c
   if (FLOW == 3 && a.basis_tab) {
     cb = reinterpret_cast<const CutBasis*>(a.basis_tab) + tile;
   } else if (need_cut) {
-    if (tid < 32) cut_basis<WIDE, C>(a, base, q, &cb_s);
+    if (tid < 32) {
+      if (WGT) {
+        if (flags & kPreCost) wbasis<C>(a, base, q, a.wu1, &wb_s[0]);
+        if (flags & kMidCost) wbasis<C>(a, base, q, a.wu2, &wb_s[WGT ? 1 : 0]);
+        if (flags & kExpect) wcut_basis<C>(a, base, q, &wcb_s[0]);
+      } else {
+        cut_basis<WIDE, C>(a, base, q, &cb_s);
+      }
+    }
     if ((flags & kPreCost) || kMB == 0) __syncthreads();
   }
   const int e = a.g.tot_edge;
   const double t1 = a.rx1.a, t2 = a.rx2.a;
   if (FLOW == 3 && (flags & kGenTab)) gen32<0>(v, cb, a.table, e, tid);
+  else if (WGT && (flags & kPreCost)) wcost32<0>(v, &wb_s[0], a.wq1, tid);
   else if (flags & kPreCost) cost32<0>(v, cb, a.table, e, tid);
   rx5<0x1Fu>(v, t1);
   if (kMB) {
@@ -272,11 +344,13 @@ __global__ void __launch_bounds__(s32::kT, S32_MINB_F(C, FLOW)) sweep32_kernel(c
   }
   if (FLOW == 2) {
     if (kMB) {
-      cost32<1>(v, cb, a.table2, e, tid);
+      if (WGT) wcost32<1>(v, &wb_s[WGT ? 1 : 0], a.wq2, tid);
+      else cost32<1>(v, cb, a.table2, e, tid);
       rx5<kMB>(v, t2);
       xchg<1, 0>(buf, tid, v);
     } else {
-      cost32<0>(v, cb, a.table2, e, tid);
+      if (WGT) wcost32<0>(v, &wb_s[WGT ? 1 : 0], a.wq2, tid);
+      else cost32<0>(v, cb, a.table2, e, tid);
     }
     rx5<0x1Fu>(v, t2);
   }
@@ -286,7 +360,7 @@ __global__ void __launch_bounds__(s32::kT, S32_MINB_F(C, FLOW)) sweep32_kernel(c
     for (int r = 0; r < kR; ++r) v[r] = cmul_np(v[r], a.scale);
   }
   double acc = 0.0;
-  if (flags & kExpect) acc = expect32<last>(v, cb, tid);
+  if (flags & kExpect) acc = WGT ? wexpect32<last>(v, &wcb_s[0], a.wc, tid) : expect32<last>(v, cb, tid);
   if (!(flags & kNoStore)) {
     if (last == 0) {
       double2* p = amps + base + toff;
@@ -326,10 +400,22 @@ static bool gen32_enabled() {
   }
   return v > 0;
 }
+// Weighted (compressed backend) fast sweeps, two CTAs per SM: N=30 weighted
+// p=10 67.2-67.6 vs 66.0-66.5 layers/s, p=4 66.7-67.3 vs 64.9 (tools/wgt32_probe.py,
+// profiles/r13_wgt32_ab.txt).  QAOA_SWEEP32_WGT=0 keeps them on 256 x 16 (A/B).
+static bool wgt32_enabled() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("QAOA_SWEEP32_WGT");
+    v = e ? atoi(e) : 1;
+  }
+  return v > 0;
+}
 static bool sweep32_supported(const SweepArgs& a) {
   if ((a.flags & kGen) && (!gen32_enabled() || (a.flags & kStage2))) return false;
-  return a.carry >= 3 && a.carry <= 7 && !(a.flags & (kExact | kWeighted | kMirror)) && !a.out &&
-         a.ntiles >= 1 && (a.flags & kStage1);
+  if ((a.flags & kWeighted) && (!wgt32_enabled() || (a.flags & kGen))) return false;
+  return a.carry >= 3 && a.carry <= 7 && !(a.flags & (kExact | kMirror)) && !a.out && a.ntiles >= 1 &&
+         (a.flags & kStage1);
 }
 bool sweep32_eligible(const SweepArgs& a) {
   if (!sweep32_supported(a)) return false;
@@ -360,7 +446,7 @@ bool sweep32_selected(const SweepArgs& a) {
   return on == 2 ? sweep32_supported(a) : (on > 0 && sweep32_eligible(a));
 }
 
-template <bool WIDE, int C, int FLOW>
+template <bool WIDE, int C, int FLOW, bool WGT = false>
 static cudaError_t launch32_one(const SweepArgs& a, int grid, cudaStream_t s) {
   constexpr int smem = kTile * (int)sizeof(double2);
   static unsigned long long configured = 0;
@@ -368,18 +454,20 @@ static cudaError_t launch32_one(const SweepArgs& a, int grid, cudaStream_t s) {
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(sweep32_kernel<WIDE, C, FLOW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         smem);
+    cudaError_t e = cudaFuncSetAttribute(sweep32_kernel<WIDE, C, FLOW, WGT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
   }
-  sweep32_kernel<WIDE, C, FLOW><<<grid, s32::kT, smem, s>>>(a);
+  sweep32_kernel<WIDE, C, FLOW, WGT><<<grid, s32::kT, smem, s>>>(a);
   return cudaGetLastError();
 }
 
 template <bool WIDE, int C>
 static cudaError_t launch32_c(const SweepArgs& a, int grid, cudaStream_t s) {
   if (a.flags & kGen) return launch32_one<WIDE, C, 3>(a, grid, s);  // launch control (FLOW 1 + kGen)
+  if (a.flags & kWeighted)
+    return (a.flags & kStage2) ? launch32_one<WIDE, C, 2, true>(a, grid, s) : launch32_one<WIDE, C, 1, true>(a, grid, s);
   return (a.flags & kStage2) ? launch32_one<WIDE, C, 2>(a, grid, s) : launch32_one<WIDE, C, 1>(a, grid, s);
 }
 
